@@ -1,0 +1,145 @@
+/*
+ * twopass.h — C ABI of libtwopass.so, a B200 (sm_100a) implementation of
+ * "The Two-Pass Softmax Algorithm" (Dukhan & Ablavatski, arXiv 2001.04438).
+ *
+ * Operation (all entry points): row-wise softmax of a row-major matrix,
+ *     y[r][i] = e^{x[r][i]} / sum_k e^{x[r][k]}                (§1)
+ * computed by Alg. 3 SoftmaxTwoPass (§4): pass 1 reads each row
+ * once, turns every x into an extended-exponent pair (m, n) with e^x = m 2^n
+ * (ExtExp) and reduces the pairs with max-exponent
+ * rescaling to (m_sum, n_sum); pass 2 re-reads the row and
+ * writes y = m * lambda_sum * 2^{n - n_sum} with lambda_sum = 1/m_sum
+ * (PAPER.md:164-168).  No max pass; no overflow for any finite input.
+ * The softmax3_* entry points are the in-house Three-Pass comparators
+ * (Alg. 1 Recompute; Alg. 2 Reload).
+ *
+ * Conventions shared by every entry point
+ *   Layout     x: rows x cols, row-major, contiguous, row stride = cols elements.
+ *              y: rows x cols fp32, same layout.  bf16 inputs are raw bf16 bit
+ *              patterns (uint16_t), converted exactly to fp32; arithmetic and
+ *              output are fp32.
+ *   Memory     x, y, pairs: DEVICE pointers (cudaMalloc / torch), owned by the
+ *              caller; the library never frees them.  Any alignment is accepted;
+ *              16-byte aligned rows (cols % 4 == 0 fp32, % 8 == 0 bf16, 16-byte
+ *              aligned bases) use 128-bit loads/stores.
+ *   Aliasing   fp32 entry points allow y == x exactly (in place); any partial
+ *              overlap of x and y is rejected.  bf16 entry points reject overlap.
+ *   Streams    Enqueue-only: the call returns after launching on `stream`
+ *              (0 = legacy default stream) without synchronising.  Execution
+ *              errors surface at the caller's next synchronisation.
+ *   Workspace  Entry points without a workspace argument use one internal
+ *              per-device workspace (allocated, zero-filled and grown on first
+ *              use; growth synchronises the device).  Calls that use it must not
+ *              run concurrently on different streams of one device; use the _ex
+ *              variants with caller-owned workspaces for that and for CUDA-graph
+ *              capture.
+ *   Accuracy   Per element, against the exact softmax o: |y - o| <= 2e-5 o for
+ *              o >= FLT_MIN, |y - o| <= 1e-37 below (BASELINE.json north_star),
+ *              for finite |x| <= 2^21 (reading G11; larger magnitudes
+ *              are clamped to +-2^21, NaN is treated as -2^21).
+ *   Determinism Results are bitwise reproducible and independent of grid size,
+ *              stream, alignment and (for the partial/finish path with a
+ *              power-of-two world and block-aligned equal chunks) of the number
+ *              of ranks (reading G8).
+ *   Status     0 TP_OK; 1 TP_EINVAL (null pointer, rows < 1 or cols < 1, partial
+ *              x/y overlap, world < 1, workspace too small); 2 TP_ECUDA (launch
+ *              or allocation error: see softmax_last_cuda_error()); 3 TP_ENODEV
+ *              (no CUDA device).  Nothing is launched when the status is not 0.
+ */
+#ifndef TWOPASS_H
+#define TWOPASS_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TP_OK = 0, TP_EINVAL = 1, TP_ECUDA = 2, TP_ENODEV = 3 };
+
+/* Algorithm and input-dtype selectors of the _ex entry points. */
+enum { TP_ALGO_TWO_PASS = 0, TP_ALGO_THREE_PASS_RECOMPUTE = 2, TP_ALGO_THREE_PASS_RELOAD = 3 };
+enum { TP_IN_F32 = 0, TP_IN_BF16 = 1 };
+
+/* ---- Two-Pass softmax (Alg. 3) -------------------------- */
+int softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream);
+int softmax_bf16_f32(const uint16_t* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream);
+
+/* ---- Three-Pass comparators: Recompute (Alg. 1) and Reload
+ *      (Alg. 2), same polynomial and range reduction as ExtExp
+ *       plus reconstruction with flush below 2^-126. */
+int softmax3_recompute_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream);
+int softmax3_reload_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream);
+int softmax3_recompute_bf16_f32(const uint16_t* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream);
+int softmax3_reload_bf16_f32(const uint16_t* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream);
+
+/* ---- Split Two-Pass for sharded rows (multi-GPU, BASELINE.json north_star) ----
+ * partial: pass 1 of Alg. 3 over a chunk of every row, reduced
+ *   to one pair per row: pair_out[2r] = m_sum, pair_out[2r+1] = n_sum (device,
+ *   rows x 2 fp32).  The chunk's pair represents sum_i e^{x_i} = m_sum 2^{n_sum}.
+ * finish: merges `world` partials per row (pairs: device, world x rows x 2 fp32,
+ *   rank-major: pairs[(w*rows + r)*2 + {0,1}]) with a balanced tree over rank index,
+ *   computes lambda_sum = 1/m_sum and runs pass 2
+ *   over the local chunk x -> y.  With world == 1 the result equals softmax_f32's
+ *   bit for bit.                                                                */
+int softmax_f32_partial(const float* x, int64_t rows, int64_t cols, float* pair_out, cudaStream_t stream);
+int softmax_bf16_partial(const uint16_t* x, int64_t rows, int64_t cols, float* pair_out, cudaStream_t stream);
+int softmax_f32_finish(const float* x, float* y, int64_t rows, int64_t cols, const float* pairs, int world,
+                       cudaStream_t stream);
+int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t cols, const float* pairs,
+                            int world, cudaStream_t stream);
+
+/* ---- explicit-workspace / tuning variants ----------------------------------
+ * workspace: device memory of at least softmax_workspace_bytes(rows, cols) bytes,
+ *   ZERO-FILLED before its first use; the kernels leave it reusable.  One
+ *   workspace must not be used by two launches running concurrently.
+ * opts: may be NULL.  grid_ctas = persistent grid size (0 = one resident wave;
+ *   larger values are clamped to it); lookahead_rows = rows of pass 1 kept ahead of
+ *   pass 2 (0 = automatic); force_persistent = use the work-queue kernel even for
+ *   rows that fit one block.  Results do not depend on any of these. */
+typedef struct {
+    int64_t grid_ctas;
+    int64_t lookahead_rows;
+    int force_persistent;
+} softmax_opts;
+
+size_t softmax_workspace_bytes(int64_t rows, int64_t cols);
+int softmax_ex(int algo, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, void* workspace,
+               size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream);
+int softmax_partial_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, float* pair_out, void* workspace,
+                       size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream);
+int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
+                      int world, const softmax_opts* opts, cudaStream_t stream);
+
+/* ---- end-to-end call on HOST buffers ---------------------------------------
+ * hx, hy: HOST pointers (pinned memory gives full PCIe bandwidth).  Copies x to
+ * the current device, runs softmax_f32 / softmax_bf16_f32, copies y back and
+ * returns when hy is filled (synchronous).  Row slabs are pipelined over two
+ * streams so host->device copies, kernels and device->host copies overlap.
+ * Device staging memory is cached per device between calls.                   */
+int softmax_f32_host(const float* hx, float* hy, int64_t rows, int64_t cols);
+int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t cols);
+
+/* ---- status ---------------------------------------------------------------- */
+const char* softmax_status_str(int status);
+int softmax_last_cuda_error(void); /* cudaError_t of the last TP_ECUDA on this thread */
+/* Watchdog flags of a workspace (NULL = this device's internal one); synchronous.
+ * Bit 0: a pass-2 block waited more than 4 s for its row's pass-1 result and gave up
+ * (a bug: the outputs of that launch are invalid).  reset != 0 clears the flags.
+ * Returns -1 on a CUDA error. */
+int softmax_watchdog_flags(const void* workspace, int reset);
+
+/* ---- unit-test hooks (device arrays of `count` fp32 values) -----------------
+ * what = 0: ExtExp(a) -> (out0 = m, out1 = n)
+ *        1: pow2_flush(a) -> out0 = 2^a or 0 (a < -126, -inf, NaN)
+ *        2: pair merge (a[2i], a[2i+1]) + (b[2i], b[2i+1]) -> (out0, out1)
+ *        3: Exp with reconstruction, argument a <= 0 -> out0 (Alg. 4) */
+int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
+                cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TWOPASS_H */

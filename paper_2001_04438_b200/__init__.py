@@ -1,0 +1,211 @@
+"""Two-Pass softmax (Dukhan & Ablavatski, arXiv 2001.04438) on B200 — Python binding.
+
+Thin ctypes marshalling over libtwopass.so (C ABI: include/twopass.h).  Every
+step of the computation runs in the library's sm_100a kernels; this module only
+passes device pointers, sizes and the current CUDA stream.  There is no CPU or
+PyTorch fallback: if the library is missing or no GPU is present, calls raise.
+
+    softmax(x)                   Alg. 3 SoftmaxTwoPass
+    softmax3_recompute(x)        Alg. 1, PAPER.md:88-104   (in-house comparator)
+    softmax3_reload(x)           Alg. 2, PAPER.md:108-128  (in-house comparator)
+    partial(x) / finish(x, pairs, world)
+                                 Alg. 3 pass 1 / pass 2 split for sharded rows
+    softmax_host(hx, hy)         end-to-end call on host buffers
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_PKG, "libtwopass.so")
+
+TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV = 0, 1, 2, 3
+ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3
+IN_F32, IN_BF16 = 0, 1
+
+EXPORTS = [
+    "softmax_f32", "softmax_bf16_f32", "softmax3_recompute_f32", "softmax3_reload_f32",
+    "softmax3_recompute_bf16_f32", "softmax3_reload_bf16_f32", "softmax_f32_partial",
+    "softmax_bf16_partial", "softmax_f32_finish", "softmax_bf16_f32_finish", "softmax_workspace_bytes",
+    "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_f32_host", "softmax_bf16_f32_host",
+    "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "tp_debug_op",
+]
+
+
+class TwoPassError(RuntimeError):
+    pass
+
+
+class SoftmaxOpts(ctypes.Structure):
+    _fields_ = [("grid_ctas", ctypes.c_int64), ("lookahead_rows", ctypes.c_int64),
+                ("force_persistent", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libtwopass.so (built by __graft_entry__.build() / paper_2001_04438_b200/build.py)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no fallback implementation)")
+        L = ctypes.CDLL(_SO)
+        vp, i64, ci, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+        for nm in ("softmax_f32", "softmax_bf16_f32", "softmax3_recompute_f32", "softmax3_reload_f32",
+                   "softmax3_recompute_bf16_f32", "softmax3_reload_bf16_f32"):
+            getattr(L, nm).argtypes = [vp, vp, i64, i64, vp]
+        for nm in ("softmax_f32_partial", "softmax_bf16_partial"):
+            getattr(L, nm).argtypes = [vp, i64, i64, vp, vp]
+        for nm in ("softmax_f32_finish", "softmax_bf16_f32_finish"):
+            getattr(L, nm).argtypes = [vp, vp, i64, i64, vp, ci, vp]
+        L.softmax_workspace_bytes.argtypes = [i64, i64]
+        L.softmax_workspace_bytes.restype = sz
+        L.softmax_ex.argtypes = [ci, ci, vp, vp, i64, i64, vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
+        L.softmax_partial_ex.argtypes = [ci, vp, i64, i64, vp, vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
+        L.softmax_finish_ex.argtypes = [ci, vp, vp, i64, i64, vp, ci, ctypes.POINTER(SoftmaxOpts), vp]
+        L.softmax_f32_host.argtypes = [vp, vp, i64, i64]
+        L.softmax_bf16_f32_host.argtypes = [vp, vp, i64, i64]
+        L.softmax_status_str.argtypes = [ci]
+        L.softmax_status_str.restype = ctypes.c_char_p
+        L.tp_debug_op.argtypes = [ci, vp, vp, vp, vp, i64, vp]
+        L.softmax_watchdog_flags.argtypes = [vp, ci]
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str) -> None:
+    if status != TP_OK:
+        msg = lib().softmax_status_str(status).decode()
+        if status == TP_ECUDA:
+            msg += f" (cudaError {lib().softmax_last_cuda_error()})"
+        raise TwoPassError(f"{what}: {msg}")
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _in_dtype(x: torch.Tensor) -> int:
+    if x.dtype == torch.float32:
+        return IN_F32
+    if x.dtype == torch.bfloat16:
+        return IN_BF16
+    raise TypeError(f"two-pass softmax takes float32 or bfloat16 logits, got {x.dtype}")
+
+
+def _rows_cols(x: torch.Tensor) -> tuple[int, int]:
+    if x.dim() == 0:
+        raise ValueError("softmax of a 0-d tensor")
+    cols = x.shape[-1]
+    rows = x.numel() // cols if cols else 0
+    return rows, cols
+
+
+def _prep(x: torch.Tensor) -> torch.Tensor:
+    if not x.is_cuda:
+        raise ValueError("x must be a CUDA tensor (use softmax_host for host buffers)")
+    return x if x.is_contiguous() else x.contiguous()
+
+
+def _opts(grid_ctas: int = 0, lookahead_rows: int = 0, force_persistent: bool = False):
+    if not (grid_ctas or lookahead_rows or force_persistent):
+        return None
+    return ctypes.pointer(SoftmaxOpts(grid_ctas, lookahead_rows, int(force_persistent)))
+
+
+def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None, grid_ctas: int = 0, lookahead_rows: int = 0,
+               force_persistent: bool = False) -> torch.Tensor:
+    """Row-wise softmax over the last dim; fp32 output.  See include/twopass.h."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
+    assert y.is_contiguous() and y.dtype == torch.float32 and y.shape == x.shape
+    ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel() *
+                                                             workspace.element_size())
+    st = lib().softmax_ex(algo, _in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, ws_ptr, ws_bytes,
+                          _opts(grid_ctas, lookahead_rows, force_persistent), _stream())
+    _check(st, "softmax")
+    return y
+
+
+def softmax(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Two-Pass softmax (Alg. 3) over the last dim of a CUDA float32/bfloat16 tensor."""
+    return softmax_ex(x, ALGO_TWO_PASS, out)
+
+
+def softmax3_recompute(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    return softmax_ex(x, ALGO_RECOMPUTE, out)
+
+
+def softmax3_reload(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    return softmax_ex(x, ALGO_RELOAD, out)
+
+
+def workspace_bytes(rows: int, cols: int) -> int:
+    return int(lib().softmax_workspace_bytes(rows, cols))
+
+
+def new_workspace(rows: int, cols: int, device=None) -> torch.Tensor:
+    """Zero-filled caller-owned workspace for the _ex entry points."""
+    return torch.zeros(max(workspace_bytes(rows, cols), 1), dtype=torch.uint8, device=device or "cuda")
+
+
+def partial(x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+            grid_ctas: int = 0) -> torch.Tensor:
+    """Pass 1 of Alg. 3 over a chunk of each row -> [rows, 2] fp32 (m_sum, n_sum)."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    p = torch.empty((rows, 2), dtype=torch.float32, device=x.device) if out is None else out
+    ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel())
+    st = lib().softmax_partial_ex(_in_dtype(x), x.data_ptr(), rows, cols, p.data_ptr(), ws_ptr, ws_bytes,
+                                  _opts(grid_ctas), _stream())
+    _check(st, "partial")
+    return p
+
+
+def finish(x: torch.Tensor, pairs: torch.Tensor, world: int, out: torch.Tensor | None = None,
+           grid_ctas: int = 0) -> torch.Tensor:
+    """Merge `world` partials per row (pairs: [world, rows, 2]) and run pass 2 on the local chunk."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    assert pairs.is_cuda and pairs.dtype == torch.float32 and pairs.is_contiguous()
+    assert pairs.numel() == world * rows * 2
+    y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
+    st = lib().softmax_finish_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, pairs.data_ptr(), world,
+                                 _opts(grid_ctas), _stream())
+    _check(st, "finish")
+    return y
+
+
+def softmax_host(hx: torch.Tensor, hy: torch.Tensor | None = None) -> torch.Tensor:
+    """End-to-end softmax of a HOST (ideally pinned) tensor into a host fp32 tensor (synchronous)."""
+    assert not hx.is_cuda and hx.is_contiguous()
+    rows, cols = _rows_cols(hx)
+    if hy is None:
+        hy = torch.empty(hx.shape, dtype=torch.float32, pin_memory=hx.is_pinned())
+    assert not hy.is_cuda and hy.is_contiguous() and hy.dtype == torch.float32
+    f = lib().softmax_f32_host if _in_dtype(hx) == IN_F32 else lib().softmax_bf16_f32_host
+    _check(f(hx.data_ptr(), hy.data_ptr(), rows, cols), "softmax_host")
+    return hy
+
+
+def watchdog_flags(workspace: torch.Tensor | None = None, reset: bool = True) -> int:
+    """Watchdog bits of a workspace (None = internal); 0 means no pass-2 wait ever timed out."""
+    return int(lib().softmax_watchdog_flags(None if workspace is None else workspace.data_ptr(), int(reset)))
+
+
+def debug_op(what: int, a: torch.Tensor, b: torch.Tensor | None = None):
+    """Unit-test hook (include/twopass.h tp_debug_op)."""
+    a = _prep(a.float())
+    count = a.numel() // 2 if what == 2 else a.numel()
+    o0 = torch.empty(count, dtype=torch.float32, device=a.device)
+    o1 = torch.empty(count, dtype=torch.float32, device=a.device)
+    bp = _prep(b.float()).data_ptr() if b is not None else None
+    _check(lib().tp_debug_op(what, a.data_ptr(), bp, o0.data_ptr(), o1.data_ptr(), count, _stream()), "debug_op")
+    return o0, o1

@@ -1,0 +1,374 @@
+// C ABI of libtwopass.so (declared and documented in include/twopass.h): argument checks,
+// the internal per-device workspace, the host-buffer (end-to-end) pipeline.  No arithmetic of
+// the method lives here; every step runs in the kernels of tp_kernels.cu.
+#include <cstring>
+#include <mutex>
+
+#include "../../include/twopass.h"
+#include "tp_internal.h"
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+int cuda_fail(cudaError_t e) {
+    g_last_cuda_error = (int)e;
+    return TP_ECUDA;
+}
+
+constexpr int kMaxDev = 64;
+
+struct DevState {
+    std::mutex mu;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    // host pipeline, row slabs: two staging slots (one per stream)
+    void* hx_dev[2] = {nullptr, nullptr};
+    float* hy_dev[2] = {nullptr, nullptr};
+    size_t stage_bytes_x = 0, stage_bytes_y = 0;
+    void* hws[2] = {nullptr, nullptr};
+    size_t hws_bytes = 0;
+    // host pipeline, single long row: whole-row buffers, chunk workspace, chunk pairs
+    void* row_x = nullptr;
+    void* row_y = nullptr;
+    size_t row_x_bytes = 0, row_y_bytes = 0;
+    void* row_ws = nullptr;
+    size_t row_ws_bytes = 0;
+    void* pairs = nullptr;
+    size_t pairs_bytes = 0;
+    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaEvent_t ev[64];
+    bool ev_init = false;
+};
+DevState g_dev[kMaxDev];
+
+int current_device(int* dev) {
+    cudaError_t e = cudaGetDevice(dev);
+    if (e != cudaSuccess) return e == cudaErrorNoDevice ? TP_ENODEV : cuda_fail(e);
+    if (*dev < 0 || *dev >= kMaxDev) return TP_EINVAL;
+    return TP_OK;
+}
+
+// Grow-only zero-filled device buffer.  Growth synchronises the device (documented).
+int ensure_zeroed(void** p, size_t* have, size_t need) {
+    if (*have >= need && *p) return TP_OK;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    e = cudaMalloc(p, need);
+    if (e != cudaSuccess) return cuda_fail(e);
+    e = cudaMemset(*p, 0, need);
+    if (e != cudaSuccess) return cuda_fail(e);
+    *have = need;
+    return TP_OK;
+}
+
+int internal_workspace(size_t need, void** ws) {
+    int dev;
+    int st = current_device(&dev);
+    if (st) return st;
+    DevState& d = g_dev[dev];
+    std::lock_guard<std::mutex> lk(d.mu);
+    st = ensure_zeroed(&d.ws, &d.ws_bytes, need < 4096 ? 4096 : need);
+    if (st) return st;
+    *ws = d.ws;
+    return TP_OK;
+}
+
+bool overlap_bad(const void* x, size_t xbytes, const void* y, size_t ybytes, bool allow_exact) {
+    const uintptr_t x0 = (uintptr_t)x, x1 = x0 + xbytes, y0 = (uintptr_t)y, y1 = y0 + ybytes;
+    if (x1 <= y0 || y1 <= x0) return false;
+    return !(allow_exact && x0 == y0 && xbytes == ybytes);
+}
+
+int check_args(int in_dtype, const void* x, const float* y, int64_t rows, int64_t cols, bool need_y) {
+    if (!x || (need_y && !y)) return TP_EINVAL;
+    if (rows < 1 || cols < 1) return TP_EINVAL;
+    if (in_dtype != TP_IN_F32 && in_dtype != TP_IN_BF16) return TP_EINVAL;
+    if (rows > (int64_t(1) << 40) / cols) return TP_EINVAL;  // 2^40 elements: far beyond HBM
+    if (need_y) {
+        const size_t esz = in_dtype == TP_IN_BF16 ? 2 : 4;
+        if (overlap_bad(x, (size_t)(rows * cols) * esz, y, (size_t)(rows * cols) * 4, in_dtype == TP_IN_F32))
+            return TP_EINVAL;
+    }
+    return TP_OK;
+}
+
+tp::LaunchOpts to_opts(const softmax_opts* o) {
+    tp::LaunchOpts L;
+    if (o) {
+        L.grid_ctas = o->grid_ctas;
+        L.lookahead_rows = o->lookahead_rows;
+        L.force_persistent = o->force_persistent;
+    }
+    return L;
+}
+
+int run_softmax(int algo, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, void* ws,
+                size_t ws_bytes, const softmax_opts* opts, cudaStream_t s) {
+    int st = check_args(in_dtype, x, y, rows, cols, true);
+    if (st) return st;
+    if (algo != TP_ALGO_TWO_PASS && algo != TP_ALGO_THREE_PASS_RECOMPUTE && algo != TP_ALGO_THREE_PASS_RELOAD)
+        return TP_EINVAL;
+    const tp::LaunchOpts lo = to_opts(opts);
+    if (tp::softmax_needs_workspace(algo, cols, lo)) {
+        const size_t need = tp::workspace_bytes(rows, cols);
+        if (ws) {
+            if (ws_bytes < need) return TP_EINVAL;
+        } else {
+            st = internal_workspace(need, &ws);
+            if (st) return st;
+        }
+    }
+    cudaError_t e = tp::launch_softmax(algo, in_dtype == TP_IN_BF16, x, y, rows, cols, ws, lo, s);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int run_partial(int in_dtype, const void* x, int64_t rows, int64_t cols, float* pair_out, void* ws,
+                size_t ws_bytes, const softmax_opts* opts, cudaStream_t s) {
+    int st = check_args(in_dtype, x, nullptr, rows, cols, false);
+    if (st) return st;
+    if (!pair_out) return TP_EINVAL;
+    const size_t need = tp::workspace_bytes(rows, cols);
+    if (ws) {
+        if (ws_bytes < need) return TP_EINVAL;
+    } else {
+        st = internal_workspace(need, &ws);
+        if (st) return st;
+    }
+    cudaError_t e = tp::launch_partial(in_dtype == TP_IN_BF16, x, rows, cols, pair_out, ws, to_opts(opts), s);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int run_finish(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs, int world,
+               const softmax_opts* opts, cudaStream_t s) {
+    int st = check_args(in_dtype, x, y, rows, cols, true);
+    if (st) return st;
+    if (!pairs || world < 1) return TP_EINVAL;
+    cudaError_t e = tp::launch_finish(in_dtype == TP_IN_BF16, x, y, rows, cols, pairs, world, to_opts(opts), s);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+// ---------------------------------------------------------------- host-buffer pipeline
+int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t cols) {
+    int st = check_args(in_dtype, hx, hy, rows, cols, true);
+    if (st) return st;
+    int dev;
+    st = current_device(&dev);
+    if (st) return st;
+    DevState& d = g_dev[dev];
+    std::lock_guard<std::mutex> lk(d.mu);
+    cudaError_t e;
+    if (!d.st[0]) {
+        for (int i = 0; i < 2; ++i) {
+            e = cudaStreamCreateWithFlags(&d.st[i], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+    }
+    if (!d.ev_init) {
+        for (auto& ev : d.ev) {
+            e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+        d.ev_init = true;
+    }
+    const size_t esz = in_dtype == TP_IN_BF16 ? 2 : 4;
+    const int64_t n = rows * cols;
+    const int64_t kBlock = 16384;  // tp::kBlockElems
+    const int64_t nb = (cols + kBlock - 1) / kBlock;
+
+    if (rows == 1 && cols % kBlock == 0 && nb >= 64) {
+        // Single long row: stream it in K equal block-aligned chunks (K a power of two, so the
+        // chunk partials merged by the finish kernel's tree reproduce softmax_f32 bit for bit).
+        int K = 32;
+        while (K > 1 && nb % K) K >>= 1;
+        const int64_t cl = cols / K;
+        if ((st = ensure_zeroed(&d.row_x, &d.row_x_bytes, (size_t)n * esz))) return st;
+        if ((st = ensure_zeroed(&d.row_y, &d.row_y_bytes, (size_t)n * 4))) return st;
+        if ((st = ensure_zeroed(&d.row_ws, &d.row_ws_bytes, tp::workspace_bytes(1, cl)))) return st;
+        if ((st = ensure_zeroed(&d.pairs, &d.pairs_bytes, sizeof(float) * 2 * K))) return st;
+        char* dx = (char*)d.row_x;
+        float* dy = (float*)d.row_y;
+        float* pairs = (float*)d.pairs;
+        cudaStream_t cp = d.st[0], cm = d.st[1];
+        const tp::LaunchOpts lo;
+        for (int c = 0; c < K; ++c) {  // H2D chunk c || pass 1 of chunk c-1
+            e = cudaMemcpyAsync(dx + (size_t)c * cl * esz, (const char*)hx + (size_t)c * cl * esz, (size_t)cl * esz,
+                                cudaMemcpyHostToDevice, cp);
+            if (e != cudaSuccess) return cuda_fail(e);
+            cudaEventRecord(d.ev[c], cp);
+            cudaStreamWaitEvent(cm, d.ev[c], 0);
+            e = tp::launch_partial(in_dtype == TP_IN_BF16, dx + (size_t)c * cl * esz, 1, cl, pairs + 2 * c,
+                                   d.row_ws, lo, cm);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+        for (int c = 0; c < K; ++c) {  // pass 2 of chunk c || D2H chunk c-1
+            e = tp::launch_finish(in_dtype == TP_IN_BF16, dx + (size_t)c * cl * esz, dy + (size_t)c * cl, 1, cl,
+                                  pairs, K, lo, cm);
+            if (e != cudaSuccess) return cuda_fail(e);
+            cudaEventRecord(d.ev[32 + c], cm);
+            cudaStreamWaitEvent(cp, d.ev[32 + c], 0);
+            e = cudaMemcpyAsync(hy + (size_t)c * cl, dy + (size_t)c * cl, (size_t)cl * 4, cudaMemcpyDeviceToHost, cp);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+        e = cudaStreamSynchronize(cp);
+        return e == cudaSuccess ? TP_OK : cuda_fail(e);
+    }
+
+    // Row slabs, double-buffered over two streams: H2D(slab i+1) overlaps kernel + D2H(slab i).
+    int64_t slab = (int64_t)((64ull << 20) / ((size_t)cols * 4));
+    if (slab < 1) slab = 1;
+    if (slab > rows) slab = rows;
+    const size_t need_x = (size_t)(slab * cols) * esz, need_y = (size_t)(slab * cols) * 4;
+    if (d.stage_bytes_x < need_x || d.stage_bytes_y < need_y || !d.hx_dev[1] || !d.hy_dev[1]) {
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(e);
+        for (int i = 0; i < 2; ++i) {
+            if (d.hx_dev[i]) cudaFree(d.hx_dev[i]);
+            if (d.hy_dev[i]) cudaFree(d.hy_dev[i]);
+            d.hx_dev[i] = nullptr;
+            d.hy_dev[i] = nullptr;
+        }
+        const size_t bx = need_x > d.stage_bytes_x ? need_x : d.stage_bytes_x;
+        const size_t by = need_y > d.stage_bytes_y ? need_y : d.stage_bytes_y;
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaMalloc(&d.hx_dev[i], bx)) != cudaSuccess) return cuda_fail(e);
+            if ((e = cudaMalloc((void**)&d.hy_dev[i], by)) != cudaSuccess) return cuda_fail(e);
+        }
+        d.stage_bytes_x = bx;
+        d.stage_bytes_y = by;
+    }
+    const tp::LaunchOpts lo;
+    const bool needs_ws = tp::softmax_needs_workspace(TP_ALGO_TWO_PASS, cols, lo);
+    if (needs_ws) {
+        const size_t wsb = tp::workspace_bytes(slab, cols);
+        if (d.hws_bytes < wsb || !d.hws[1]) {
+            e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return cuda_fail(e);
+            for (int i = 0; i < 2; ++i) {
+                if (d.hws[i]) cudaFree(d.hws[i]);
+                if ((e = cudaMalloc(&d.hws[i], wsb)) != cudaSuccess) return cuda_fail(e);
+                if ((e = cudaMemset(d.hws[i], 0, wsb)) != cudaSuccess) return cuda_fail(e);
+            }
+            d.hws_bytes = wsb;
+        }
+    }
+    for (int64_t r0 = 0, i = 0; r0 < rows; r0 += slab, ++i) {
+        const int k = (int)(i & 1);
+        const int64_t nr = rows - r0 < slab ? rows - r0 : slab;
+        cudaStream_t s = d.st[k];
+        e = cudaMemcpyAsync(d.hx_dev[k], (const char*)hx + (size_t)(r0 * cols) * esz, (size_t)(nr * cols) * esz,
+                            cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        e = tp::launch_softmax(TP_ALGO_TWO_PASS, in_dtype == TP_IN_BF16, d.hx_dev[k], d.hy_dev[k], nr, cols,
+                               d.hws[k], lo, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        e = cudaMemcpyAsync(hy + (size_t)(r0 * cols), d.hy_dev[k], (size_t)(nr * cols) * 4, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    for (int i = 0; i < 2; ++i) {
+        e = cudaStreamSynchronize(d.st[i]);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    return TP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream) {
+    return run_softmax(TP_ALGO_TWO_PASS, TP_IN_F32, x, y, rows, cols, nullptr, 0, nullptr, stream);
+}
+int softmax_bf16_f32(const uint16_t* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream) {
+    return run_softmax(TP_ALGO_TWO_PASS, TP_IN_BF16, x, y, rows, cols, nullptr, 0, nullptr, stream);
+}
+int softmax3_recompute_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream) {
+    return run_softmax(TP_ALGO_THREE_PASS_RECOMPUTE, TP_IN_F32, x, y, rows, cols, nullptr, 0, nullptr, stream);
+}
+int softmax3_reload_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream) {
+    return run_softmax(TP_ALGO_THREE_PASS_RELOAD, TP_IN_F32, x, y, rows, cols, nullptr, 0, nullptr, stream);
+}
+int softmax3_recompute_bf16_f32(const uint16_t* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream) {
+    return run_softmax(TP_ALGO_THREE_PASS_RECOMPUTE, TP_IN_BF16, x, y, rows, cols, nullptr, 0, nullptr, stream);
+}
+int softmax3_reload_bf16_f32(const uint16_t* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream) {
+    return run_softmax(TP_ALGO_THREE_PASS_RELOAD, TP_IN_BF16, x, y, rows, cols, nullptr, 0, nullptr, stream);
+}
+int softmax_f32_partial(const float* x, int64_t rows, int64_t cols, float* pair_out, cudaStream_t stream) {
+    return run_partial(TP_IN_F32, x, rows, cols, pair_out, nullptr, 0, nullptr, stream);
+}
+int softmax_bf16_partial(const uint16_t* x, int64_t rows, int64_t cols, float* pair_out, cudaStream_t stream) {
+    return run_partial(TP_IN_BF16, x, rows, cols, pair_out, nullptr, 0, nullptr, stream);
+}
+int softmax_f32_finish(const float* x, float* y, int64_t rows, int64_t cols, const float* pairs, int world,
+                       cudaStream_t stream) {
+    return run_finish(TP_IN_F32, x, y, rows, cols, pairs, world, nullptr, stream);
+}
+int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t cols, const float* pairs, int world,
+                            cudaStream_t stream) {
+    return run_finish(TP_IN_BF16, x, y, rows, cols, pairs, world, nullptr, stream);
+}
+size_t softmax_workspace_bytes(int64_t rows, int64_t cols) {
+    if (rows < 1 || cols < 1) return 0;
+    return tp::workspace_bytes(rows, cols);
+}
+int softmax_ex(int algo, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, void* workspace,
+               size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream) {
+    if (!workspace && workspace_bytes) return TP_EINVAL;
+    return run_softmax(algo, in_dtype, x, y, rows, cols, workspace, workspace_bytes, opts, stream);
+}
+int softmax_partial_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, float* pair_out, void* workspace,
+                       size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream) {
+    return run_partial(in_dtype, x, rows, cols, pair_out, workspace, workspace_bytes, opts, stream);
+}
+int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
+                      int world, const softmax_opts* opts, cudaStream_t stream) {
+    return run_finish(in_dtype, x, y, rows, cols, pairs, world, opts, stream);
+}
+int softmax_f32_host(const float* hx, float* hy, int64_t rows, int64_t cols) {
+    return host_pipeline(TP_IN_F32, hx, hy, rows, cols);
+}
+int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t cols) {
+    return host_pipeline(TP_IN_BF16, hx, hy, rows, cols);
+}
+const char* softmax_status_str(int status) {
+    switch (status) {
+        case TP_OK: return "ok";
+        case TP_EINVAL: return "invalid argument";
+        case TP_ECUDA: return "CUDA error";
+        case TP_ENODEV: return "no CUDA device";
+        default: return "unknown status";
+    }
+}
+int softmax_last_cuda_error(void) { return g_last_cuda_error; }
+
+int softmax_watchdog_flags(const void* workspace, int reset) {
+    const void* ws = workspace;
+    if (!ws) {
+        int dev;
+        if (current_device(&dev)) return -1;
+        ws = g_dev[dev].ws;
+        if (!ws) return 0;
+    }
+    tp::WsHeader h;
+    if (cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    if (reset && h.error) {
+        unsigned z = 0;
+        cudaMemcpy((char*)ws + offsetof(tp::WsHeader, error), &z, sizeof(z), cudaMemcpyHostToDevice);
+    }
+    return (int)h.error;
+}
+
+int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
+                cudaStream_t stream) {
+    if (count < 0 || what < 0 || what > 3 || (count > 0 && (!a || !out0))) return TP_EINVAL;
+    if ((what == 0 || what == 2) && count > 0 && !out1) return TP_EINVAL;
+    if (what == 2 && count > 0 && !b) return TP_EINVAL;
+    cudaError_t e = tp::launch_debug(what, a, b, out0, out1, count, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+}  // extern "C"

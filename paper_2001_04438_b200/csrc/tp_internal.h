@@ -1,0 +1,43 @@
+// Internal (C++) interface between the C ABI (tp_api.cu) and the kernels (tp_kernels.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tp {
+
+// Workspace header: the persistent kernels' work queue and launch epoch.  Zero-filled once at
+// allocation; every launch leaves it reusable (the last CTA resets the queue).
+struct WsHeader {
+    unsigned long long counter;  // next work item
+    unsigned exit_ticket;        // CTAs that left the kernel
+    unsigned epoch;              // launches completed; row flags are valid when == epoch + 1
+    unsigned error;              // watchdog: bit 0 = a wait for a row flag timed out
+};
+
+constexpr unsigned long long kWaitTimeoutNs = 4000000000ull;  // 4 s: only a bug can wait this long
+
+struct WsLayout {
+    size_t block_vals, group_vals, group_tickets, row_tickets, row_stats, row_ready, bytes;
+};
+
+struct LaunchOpts {
+    int64_t grid_ctas = 0;       // 0 = one full wave of resident CTAs
+    int64_t lookahead_rows = 0;  // 0 = automatic
+    int force_persistent = 0;    // use the persistent kernel even for single-block rows
+};
+
+size_t workspace_bytes(int64_t rows, int64_t cols);
+bool softmax_needs_workspace(int algo, int64_t cols, const LaunchOpts& o);
+cudaError_t launch_softmax(int algo, int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, void* ws,
+                           const LaunchOpts& o, cudaStream_t s);
+cudaError_t launch_partial(int in_bf16, const void* x, int64_t rows, int64_t cols, float* pair_out, void* ws,
+                           const LaunchOpts& o, cudaStream_t s);
+cudaError_t launch_finish(int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
+                          int world, const LaunchOpts& o, cudaStream_t s);
+
+// debug / unit-test kernels (tp_debug.cu)
+cudaError_t launch_debug(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
+                         cudaStream_t s);
+
+}  // namespace tp

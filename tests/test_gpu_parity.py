@@ -1,0 +1,261 @@
+"""GPU parity of the Two-Pass softmax (and Three-Pass comparators) against the oracle.
+
+Every test calls the CUDA path through the C ABI (paper_2001_04438_b200 ctypes
+binding) and grades element by element with oracle.check (rel 2e-5 for oracle
+outputs >= FLT_MIN, abs 1e-37 below; BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from gpu_helpers import assert_parity, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_2001_04438_b200")
+
+ALGOS = {
+    "two_pass": tp.ALGO_TWO_PASS,
+    "recompute": tp.ALGO_RECOMPUTE,
+    "reload": tp.ALGO_RELOAD,
+}
+
+
+# ------------------------------------------------------------------ configurations 1-4 (full size)
+
+@pytest.mark.parametrize("algo", list(ALGOS))
+@pytest.mark.parametrize("key", ["c1", "c2", "c3"])
+def test_config_parity(key, algo):
+    x = workloads.generate(key)
+    y = to_host(tp.softmax_ex(to_dev(x), ALGOS[algo]))
+    r = assert_parity(x, y, f"{key}/{algo}")
+    assert r.n_rel > 0
+    assert abs(r.y_sum - x.shape[0]) <= 2e-5 * x.shape[0]
+
+
+@pytest.mark.parametrize("algo", list(ALGOS))
+@pytest.mark.parametrize("key", ["c4", "c4b"])
+def test_config4_parity(key, algo):
+    x = workloads.generate(key)
+    y = to_host(tp.softmax_ex(to_dev(x), ALGOS[algo]))
+    assert_parity(x, y, f"{key}/{algo}")
+
+
+def test_config1_naive_overflows_but_two_pass_is_finite():
+    # PAPER.md:76 / SPEC.md:407: a naive fp32 softmax of config 1 is inf/NaN
+    x = workloads.generate("c1")
+    xt = to_dev(x)
+    naive = torch.exp(xt) / torch.exp(xt).sum()
+    assert not bool(torch.isfinite(naive).all())
+    y = tp.softmax(xt)
+    assert bool(torch.isfinite(y).all())
+
+
+# ------------------------------------------------------------------ config 5 (2^31 elements), sampled
+
+@pytest.mark.slow
+def test_config5_full_size_sampled():
+    cfg = workloads.CONFIGS["c5"]
+    n = cfg.cols
+    host = torch.empty((1, n), dtype=torch.float32, pin_memory=True)
+    x = host.numpy()
+    workloads.generate("c5", out=x)
+    xd = host.cuda(non_blocking=True)
+    y = tp.softmax(xd)
+    # sampled outputs + whole first/last blocks + block boundaries
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 1 << 22), np.arange(0, 65536),
+                                    np.arange(n - 65536, n),
+                                    (np.arange(1, 1 << 10) * (n >> 10))]))
+    ys = y[0, torch.from_numpy(idx).cuda()].cpu().numpy()
+    ties = x[0] == x[0].max()
+    stats = oracle.row_stats(x[0])                     # full-row oracle statistics
+    r = oracle.check(np.ascontiguousarray(x[0, idx]), ys, stats)
+    assert r.ok, (r.n_bad, r.max_rel, r.max_abs)
+    assert r.n_rel > 10000                             # the tie elements sit in the relative branch
+    # property at full size: sum of y = 1 and every tie gets the same value
+    total = float(y.double().sum())
+    assert abs(total - 1.0) <= 2e-5
+    yt = y[0, torch.from_numpy(np.nonzero(ties)[0][:100000]).cuda()]
+    assert float(yt.max()) == float(yt.min())
+    del xd, y
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ ragged shapes and dtypes
+
+RAGGED = [(1, 1), (1, 2), (3, 3), (2, 5), (4, 17), (1, 1000), (7, 4095), (3, 4096), (5, 4097),
+          (2, 16383), (2, 16384), (2, 16385), (3, 32773), (1, 65537), (2, 200003), (1, 16384 * 64 + 1),
+          (1, 16384 * 65), (3, 16384 * 130 + 7), (300, 33)]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", RAGGED)
+def test_ragged_two_pass(rows, cols, dtype):
+    x = workloads.ragged_case(rows, cols, -300.0, 300.0, seed=rows, stream=cols)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    y = to_host(tp.softmax(to_dev(x)))
+    assert_parity(x, y, f"{rows}x{cols}/{dtype}")
+
+
+@pytest.mark.parametrize("algo", ["recompute", "reload"])
+@pytest.mark.parametrize("rows,cols", [(1, 1), (3, 17), (2, 16385), (1, 16384 * 65 + 3), (5, 4097)])
+def test_ragged_three_pass(rows, cols, algo):
+    x = workloads.ragged_case(rows, cols, -300.0, 300.0, seed=rows, stream=cols + 1)
+    y = to_host(tp.softmax_ex(to_dev(x), ALGOS[algo]))
+    assert_parity(x, y, f"{rows}x{cols}/{algo}")
+
+
+@pytest.mark.parametrize("cols", [1000, 4097, 50001])
+def test_misaligned_rows(cols):
+    # a view starting one element into the buffer: no 16-byte alignment anywhere
+    base = workloads.ragged_case(1, 3 * cols + 1, -50, 50, seed=9, stream=cols)[0]
+    xd = to_dev(base)[1:].view(3, cols)
+    assert xd.data_ptr() % 16 != 0
+    y = to_host(tp.softmax(xd))
+    assert_parity(base[1:].reshape(3, cols), y, "misaligned")
+    # and the aligned copy gives the same bits (per-thread assignment does not depend on alignment)
+    y2 = to_host(tp.softmax(xd.contiguous().clone()))
+    assert np.array_equal(y, y2)
+
+
+# ------------------------------------------------------------------ edge cases and contracts
+
+def test_empty_and_invalid_inputs():
+    L = tp.lib()
+    x = torch.zeros(4, device="cuda")
+    y = torch.zeros(4, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.softmax_f32(x.data_ptr(), y.data_ptr(), 0, 4, s) == tp.TP_EINVAL
+    assert L.softmax_f32(x.data_ptr(), y.data_ptr(), 1, 0, s) == tp.TP_EINVAL
+    assert L.softmax_f32(None, y.data_ptr(), 1, 4, s) == tp.TP_EINVAL
+    assert L.softmax_f32(x.data_ptr(), x.data_ptr() + 4, 1, 3, s) == tp.TP_EINVAL   # partial overlap
+    assert L.softmax_f32_finish(x.data_ptr(), y.data_ptr(), 1, 4, x.data_ptr(), 0, s) == tp.TP_EINVAL
+    with pytest.raises(tp.TwoPassError):
+        tp.softmax(torch.zeros(0, 5, device="cuda"))
+
+
+@pytest.mark.parametrize("cols", [1000, 40000])
+def test_in_place(cols):
+    x = workloads.ragged_case(3, cols, -90, 90, seed=1, stream=2)
+    xd = to_dev(x)
+    tp.softmax(xd, out=xd)
+    assert_parity(x, to_host(xd), "in-place")
+
+
+@pytest.mark.parametrize("n", [1000, 32768, 1 << 20, 1 << 24])
+def test_constant_zero_row_is_exactly_rn32_one_over_n(n):
+    # P10: m_i = 1, n_i = 0, m_sum = N exactly, lambda = RN32(1/N) -> every output == RN32(1/N)
+    y = to_host(tp.softmax(torch.zeros(1, n, device="cuda")))
+    assert np.all(y == np.float32(1.0 / n))
+
+
+def test_constant_nonzero_row():
+    for c in [88.0, -1e4, 1e4, 3.25]:
+        x = np.full((2, 70000), c, np.float32)
+        assert_parity(x, to_host(tp.softmax(to_dev(x))), f"const {c}")
+
+
+def test_extreme_magnitudes_stay_finite():
+    x = np.float32([[1e4, -1e4, 0.0, 1e4], [3.4e38, -3.4e38, 0.0, 1.0], [-3.4e38, -3.4e38, -3.4e38, -3.4e38]])
+    y = to_host(tp.softmax(to_dev(x)))
+    assert np.all(np.isfinite(y)) and np.all(y >= 0)
+    assert_parity(x[:1], y[:1], "±1e4")
+    assert np.allclose(y.sum(1), 1.0, atol=2e-5)
+
+
+def test_flush_boundary_rows():
+    # reading G9 / SURVEY M11: two-element rows [x_max, x_max - d] with d just around the
+    # FLT_MIN boundary of the smaller output; lambda' = 0.5 / m_sum keeps those outputs exact
+    xm = workloads.uniform(400, -1e4, 1e4, seed=21, stream=1).astype(np.float32)
+    rows = []
+    for d in np.arange(87.30, 87.40, 0.0025):
+        rows.append(np.stack([xm, (xm - np.float32(d)).astype(np.float32)], 1))
+    x = np.concatenate(rows).astype(np.float32)
+    y = to_host(tp.softmax(to_dev(x)))
+    r = assert_parity(x, y, "flush boundary")
+    assert r.n_rel > 0 and r.n_abs > 0
+
+
+def test_integer_shift_invariance_within_tolerance():
+    rng = np.random.default_rng(3)
+    x = rng.integers(-2000, 2000, size=(4, 30000)).astype(np.float32)
+    y0 = to_host(tp.softmax(to_dev(x)))
+    for c in [1.0, -777.0, 4096.0]:
+        xc = (x + np.float32(c)).astype(np.float32)
+        yc = to_host(tp.softmax(to_dev(xc)))
+        assert_parity(xc, yc, "shift")
+        big = y0 > 1e-30
+        assert np.max(np.abs(yc[big] - y0[big]) / y0[big]) <= 4e-5
+
+
+# ------------------------------------------------------------------ determinism (reading G8, pin P9)
+
+def test_bitwise_deterministic_across_grid_and_lookahead():
+    x = workloads.ragged_case(9, 16384 * 5 + 11, -500, 500, seed=4, stream=4)
+    xd = to_dev(x)
+    ref = to_host(tp.softmax(xd))
+    assert np.array_equal(ref, to_host(tp.softmax(xd)))
+    for g, la in [(1, 0), (7, 1), (148, 2), (1000, 0), (37, 9)]:
+        assert np.array_equal(ref, to_host(tp.softmax_ex(xd, grid_ctas=g, lookahead_rows=la))), (g, la)
+
+
+def test_rowblock_and_persistent_paths_agree_bitwise():
+    for cols in [1, 1000, 16384]:
+        xd = to_dev(workloads.ragged_case(5, cols, -100, 100, seed=5, stream=cols))
+        a = to_host(tp.softmax(xd))
+        b = to_host(tp.softmax_ex(xd, force_persistent=True))
+        assert np.array_equal(a, b), cols
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_partial_finish_world_invariance(dtype):
+    # one long row split into W equal block-aligned chunks: partial per chunk, finish with all
+    # W pairs -> bit-identical to the single-call result for W in {1, 2, 4, 8} (pin P9)
+    n = 16384 * 256
+    x = workloads.uniform(n, -1e4, 1e4, seed=8, stream=8).reshape(1, n)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    ref = to_host(tp.softmax(xd))
+    assert_parity(x, ref, "single call")
+    for W in [1, 2, 4, 8]:
+        c = n // W
+        chunks = [xd[:, w * c:(w + 1) * c].contiguous() for w in range(W)]
+        pairs = torch.stack([tp.partial(ch) for ch in chunks])        # [W, rows, 2]
+        ys = [tp.finish(ch, pairs, W) for ch in chunks]
+        y = to_host(torch.cat(ys, dim=1))
+        assert np.array_equal(y, ref), W
+
+
+def test_partial_pair_represents_row_sum():
+    # the chunk pair is (m_sum, n_sum) with m_sum 2^n_sum = sum_i e^{x_i}
+    x = workloads.ragged_case(3, 100000, -2000, 2000, seed=2, stream=6)
+    p = to_host(tp.partial(to_dev(x)))
+    for r in range(3):
+        mu, S = oracle.row_stats(x[r])
+        # log of the represented sum vs log of mu-shifted oracle sum: n ln2 + ln m = mu + ln S
+        lhs = p[r, 1] * np.log(2.0) + np.log(p[r, 0])
+        rhs = mu + float(np.log(S))
+        assert abs(lhs - rhs) <= 2e-5 * max(1.0, abs(rhs)) + 2e-5
+
+
+# ------------------------------------------------------------------ end-to-end host path
+
+@pytest.mark.parametrize("key", ["c2", "c3"])
+def test_host_pipeline_matches_device_path(key):
+    x = workloads.generate(key)
+    hx = torch.from_numpy(x).pin_memory()
+    hy = tp.softmax_host(hx)
+    ref = to_host(tp.softmax(to_dev(x)))
+    assert np.array_equal(hy.numpy(), ref)
+
+
+def test_host_pipeline_bf16_and_multi_slab():
+    x = workloads.generate("c4b", 0, 40)
+    hx = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
+    hy = tp.softmax_host(hx)
+    assert_parity(x, hy.numpy(), "host bf16")

@@ -1,0 +1,134 @@
+"""GPU unit parity of the device building blocks (tp_debug_op through the C ABI).
+
+ExtExp and Exp against their plain definitions (oracle, long double); pow2_flush
+exhaustively; the pair merge against exact rational arithmetic.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from oracle import algorithms as alg
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_2001_04438_b200")
+
+
+def _extexp(x):
+    m, n = tp.debug_op(0, torch.from_numpy(np.asarray(x, np.float32)).cuda())
+    torch.cuda.synchronize()
+    return m.cpu().numpy(), n.cpu().numpy()
+
+
+def _sweep():
+    table = [0.0, 1.0, -1.0, 10.0, 100.0, -100.0, 200.0, -200.0, 1000.0, -1000.0, 1e4, -1e4,
+             88.72283935546875, -103.97207641601562, 0.6931471824645996, 1e-30, -1e-30]
+    # near-ties of x*log2e = k + 1/2
+    ties = [(k + 0.5) * math.log(2) for k in range(-200, 200)]
+    rnd = [workloads.uniform(200000, -1e4, 1e4, seed=11, stream=1),
+           workloads.uniform(200000, -100, 100, seed=11, stream=2),
+           workloads.uniform(50000, -1, 1, seed=11, stream=3)]
+    return np.concatenate([np.asarray(table + ties, np.float32)] + rnd).astype(np.float32)
+
+
+def test_extexp_pair_represents_exp():
+    # (m, n) with m * 2^n = e^x; m within the polynomial's accuracy
+    x = _sweep()
+    m, n = _extexp(x)
+    assert np.all(n == np.rint(n))
+    want = oracle.exp_scaled(x, n.astype(np.float64))      # e^x 2^-n in long double
+    rel = np.abs((m.astype(np.longdouble) - want) / want).astype(np.float64)
+    assert rel.max() <= 3.0e-7, rel.max()
+    # n is the nearest integer to x log2 e up to the fp32 rounding of log2 e (reading G1)
+    dev = np.abs(n.astype(np.float64) - x.astype(np.float64) / math.log(2))
+    assert np.all(dev <= 0.5 + 4e-8 * np.abs(x) + 1e-12)
+    assert m.min() >= 0.70 and m.max() <= 1.42
+
+
+def test_extexp_exact_points():
+    m, n = _extexp([0.0, 1e4, -1e4, 200.0])
+    assert m[0] == 1.0 and n[0] == 0.0            # fma(p, 0, 1) = 1 exactly
+    ref_m, ref_n = oracle.extexp(np.float32([1e4, -1e4, 200.0]))
+    assert np.array_equal(n[1:], ref_n.astype(np.float32))
+    np.testing.assert_allclose(m[1:], ref_m.astype(np.float64), rtol=3e-7)
+
+
+def test_extexp_clamped_domain():
+    # |x| up to 2^21 stays accurate to 2e-5 (reading G11); beyond it outputs stay finite
+    x = np.concatenate([workloads.uniform(100000, -2.0 ** 21, 2.0 ** 21, seed=3, stream=8),
+                        np.float32([3.4e38, -3.4e38, 1e30, -1e30])]).astype(np.float32)
+    m, n = _extexp(x)
+    assert np.all(np.isfinite(m)) and np.all(np.isfinite(n)) and m.min() > 0
+    inside = np.abs(x) <= 2.0 ** 21
+    want = oracle.exp_scaled(x[inside], n[inside].astype(np.float64))
+    rel = np.abs((m[inside].astype(np.longdouble) - want) / want).astype(np.float64)
+    assert rel.max() <= 2e-5
+
+
+def test_pow2_flush_exhaustive():
+    k = np.concatenate([np.arange(-300, 2, dtype=np.float32), np.float32([-np.inf, np.nan])])
+    s, _ = tp.debug_op(1, torch.from_numpy(k).cuda())
+    s = s.cpu().numpy()
+    for ki, si in zip(k[:-2], s[:-2]):
+        want = 0.0 if ki < -126 else math.ldexp(1.0, int(ki))   # PAPER.md:252-258 (reading G5)
+        assert si == np.float32(want), (ki, si)
+    assert s[-2] == 0.0 and s[-1] == 0.0                         # identity and NaN (reading G6)
+
+
+def _merge(a, b):
+    a = torch.from_numpy(np.asarray(a, np.float32).reshape(-1)).cuda()
+    b = torch.from_numpy(np.asarray(b, np.float32).reshape(-1)).cuda()
+    m, n = tp.debug_op(2, a, b)
+    return m.cpu().numpy(), n.cpu().numpy()
+
+
+def test_pair_merge_examples():
+    # SPEC.md:48-59 examples, exact
+    inf = np.inf
+    A = [[0, -inf], [1, 3], [1.5, 10], [1, 128], [0, -inf], [1, 0]]
+    B = [[1, 5], [1, 3], [1, 0], [1, -128], [0, -inf], [1, 0]]
+    m, n = _merge(A, B)
+    assert (m[0], n[0]) == (1.0, 5.0)
+    assert (m[1], n[1]) == (2.0, 3.0)
+    assert m[2] == np.float32(1.5 + 2.0 ** -10) and n[2] == 10.0
+    assert (m[3], n[3]) == (1.0, 128.0)
+    assert m[4] == 0.0 and n[4] == -np.inf                      # identity + identity (no NaN)
+    assert (m[5], n[5]) == (2.0, 0.0)
+
+
+def test_pair_merge_random_vs_exact():
+    rng = np.random.default_rng(7)
+    K = 20000
+    ma = rng.uniform(0.7, 3000, K).astype(np.float32)
+    mb = rng.uniform(0.7, 3000, K).astype(np.float32)
+    na = rng.integers(-200, 200, K).astype(np.float32)
+    nb = (na + rng.integers(-40, 40, K)).astype(np.float32)
+    m, n = _merge(np.stack([ma, na], 1), np.stack([mb, nb], 1))
+    assert np.array_equal(n, np.maximum(na, nb))
+    for i in range(0, K, 7):
+        v, nm = alg.pair_merge_exact((float(ma[i]), float(na[i])), (float(mb[i]), float(nb[i])))
+        exact = alg.mantissa_exact(v, nm)
+        ulp = Fraction(math.ulp(float(np.float32(float(exact)))) ) * Fraction(2 ** 29)  # fp64 ulp -> fp32 ulp
+        err = abs(Fraction(float(m[i])) - exact)
+        assert err <= ulp / 2 + Fraction(1, 2 ** 60), (i, float(err), float(ulp))
+
+
+def test_exp_with_reconstruction_ulp():
+    # Alg. 4 on d <= 0: within 3 ulp of e^d where the result is normal,
+    # flushed to 0 when n < -126
+    d = np.concatenate([workloads.uniform(300000, -87.3, 0.0, seed=5, stream=5),
+                        np.float32([0.0, -1.0, -50.0, -87.33, -103.9, -104.0, -200.0, -1e4])]).astype(np.float32)
+    e, _ = tp.debug_op(3, torch.from_numpy(d).cuda())
+    e = e.cpu().numpy()
+    true = oracle.exp_scaled(d, np.zeros(d.size))              # plain e^d, long double
+    normal = true >= np.longdouble(np.finfo(np.float32).tiny)
+    ulp = np.array([math.ulp(float(np.float32(t))) * 2 ** 29 for t in true[normal].astype(np.float64)])
+    err = np.abs(e[normal].astype(np.longdouble) - true[normal]).astype(np.float64) / ulp
+    assert err.max() <= 3.0, err.max()
+    assert np.all(e[~normal] <= np.float32(np.finfo(np.float32).tiny))
+    assert e[-1] == 0.0 and e[-2] == 0.0
