@@ -1,0 +1,391 @@
+"""Benchmark of the Two-Pass softmax hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4] [--impl ours|reference]
+
+One step = one pass of the whole hot path (Alg. 3 pass 1 + pass 2) over
+one batch of the workload, inputs resident in HBM.  Metric = BASELINE.json's: achieved HBM
+GB/s under the paper's cost model (2 reads + 1 write = 12 B per fp32 element, PAPER.md
+Table 2 l.180-198), whole job.  Default workload: config 4 (256 x 800,000 fp32 rows,
+BASELINE.json configs[3]), rows sharded, one full batch per rank (weak scaling).  Inputs are
+819 MB per rank > 126 MB L2, so no explicit L2 flush is needed between steps.
+
+N > 1: launched by torchrun (one rank per GPU, NCCL).  Timing: W warm-up steps, then a
+barrier + synchronize, K steps between CUDA events on the launching stream, synchronize +
+barrier, max over ranks.  Rank 0 prints one JSON line.
+
+--impl reference: the reference arm for this tier is the oracle (oracle/, plain C, fp64 /
+long double) on the host cores, rank 0 only, each step a bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "two-pass softmax HBM GB/s and % of peak, vs three-pass, at 1/2/4/8 B200"
+BYTES_PER_ELEM = {("two_pass", "f32"): 12, ("recompute", "f32"): 16, ("reload", "f32"): 20,
+                  ("two_pass", "bf16"): 8, ("recompute", "bf16"): 10, ("reload", "bf16"): 16}
+NOMINAL_HBM_GBS = 8000.0
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks sampler
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons every 100 ms while running (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workloads
+
+def workload_spec(key: str, world: int, rank: int, scaling: str):
+    """(description, rows, cols, dtype, generator(out_array) for this rank, elements this rank)."""
+    import workloads
+    from paper_2001_04438_b200 import dist as tpd
+    cfg = workloads.CONFIGS[key]
+    if cfg.rows == 1:
+        # single long row: contiguous block-aligned chunks, one (m, n) all_gather (strong scaling)
+        c0, c1 = tpd.chunk_range(cfg.cols, world, rank)
+        gen = (lambda out, c0=c0, c1=c1: workloads.generate(key, col0=c0, ncols=c1 - c0, out=out))
+        return dict(desc=f"{key}: 1x{cfg.cols} {cfg.dtype} single row, {cfg.desc}, chunk-sharded",
+                    rows=1, cols=c1 - c0, dtype=cfg.dtype, gen=gen, scaling="strong", mode="chunk",
+                    full_cols=cfg.cols)
+    if scaling == "strong":
+        r0, r1 = tpd.row_range(cfg.rows, world, rank)
+        gen = (lambda out, r0=r0, r1=r1: workloads.generate(key, row0=r0, nrows=r1 - r0, out=out))
+        return dict(desc=f"{key}: {cfg.rows}x{cfg.cols} {cfg.dtype} total, rows sharded", rows=r1 - r0,
+                    cols=cfg.cols, dtype=cfg.dtype, gen=gen, scaling="strong", mode="rows")
+    # weak: every rank processes one full batch of the config (rank r uses seed r; rank 0 = the config)
+    gen = (lambda out, s=rank: workloads.generate(key, seed=s, out=out))
+    return dict(desc=f"{key}: {cfg.rows}x{cfg.cols} {cfg.dtype} per rank, {cfg.desc}, rows sharded",
+                rows=cfg.rows, cols=cfg.cols, dtype=cfg.dtype, gen=gen, scaling="weak", mode="rows")
+
+
+# ---------------------------------------------------------------- reference arm (oracle on CPU)
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    import workloads
+    spec = workload_spec(args.workload, 1, 0, args.scaling)
+    cfg = workloads.CONFIGS[args.workload]
+    kind = cfg.dtype
+    per_elem = BYTES_PER_ELEM[("two_pass", kind)]
+    # one step = oracle softmax over S rows (or an S*2^20-element chunk of a single row)
+    if spec["mode"] == "rows":
+        probe = workloads.generate(args.workload, row0=0, nrows=1)
+        oracle.softmax(probe)  # loads the library
+        t0 = time.perf_counter()
+        oracle.softmax(probe)
+        t_row = time.perf_counter() - t0
+        S = int(max(1, min(spec["rows"], round(args.ref_step_s / max(t_row, 1e-6)))))
+        x = workloads.generate(args.workload, row0=0, nrows=S)
+        sample = f"{S} of {spec['rows']} rows of {args.workload} per step"
+    else:
+        n = min(spec["cols"], 1 << 24)
+        x = workloads.generate(args.workload, col0=0, ncols=n)
+        t0 = time.perf_counter()
+        oracle.softmax(x)
+        t1 = time.perf_counter() - t0
+        n = int(min(spec["cols"], max(1 << 16, n * args.ref_step_s / max(t1, 1e-6))))
+        x = workloads.generate(args.workload, col0=0, ncols=n)
+        sample = f"first {n} elements of the {args.workload} row per step"
+    for _ in range(args.warmup):
+        oracle.softmax(x)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.softmax(x)
+    dt = (time.perf_counter() - t0) / args.steps
+    elems = x.size
+    value = per_elem * elems / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": spec["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": spec["desc"], "sample": sample, "bytes_per_element": per_elem},
+            "elements_per_s": elems / dt,
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": oracle.threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, spec):
+    """The oracle as it stands on this host's cores, bounded sample (~10-20 s of CPU work)."""
+    import oracle
+    import workloads
+    per_elem = BYTES_PER_ELEM[("two_pass", spec["dtype"])]
+    if spec["mode"] == "rows":
+        x = workloads.generate(args.workload, row0=0, nrows=1)
+    else:
+        x = workloads.generate(args.workload, col0=0, ncols=min(spec["cols"], 1 << 22))
+    t0 = time.perf_counter()
+    oracle.softmax(x)
+    t1 = time.perf_counter() - t0
+    reps = int(max(1, min(200, args.cpu_budget_s / max(t1, 1e-6))))
+    if spec["mode"] == "rows":
+        S = min(spec["rows"], reps)
+        x = workloads.generate(args.workload, row0=0, nrows=S)
+        sample = f"oracle softmax of {S} rows x {spec['cols']} of {args.workload}"
+    else:
+        n = int(min(spec.get("full_cols", spec["cols"]), x.size * reps))
+        x = workloads.generate(args.workload, col0=0, ncols=n)
+        sample = f"oracle softmax of the first {n} elements of the {args.workload} row"
+    t0 = time.perf_counter()
+    oracle.softmax(x)
+    dt = time.perf_counter() - t0
+    return {"value": per_elem * x.size / dt / 1e9, "unit": "GB/s", "cores": oracle.threads(), "kind": "oracle",
+            "sample": sample, "elements_per_s": x.size / dt}
+
+
+# ---------------------------------------------------------------- our arm
+
+def traffic_from_profiles(workload: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get(workload)
+    return None if d is None else d.get("dram_bytes_per_launch")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--clock-window-s", type=float, default=1.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=8.0)
+    ap.add_argument("--ref-step-s", type=float, default=1.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-three-pass", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and world == 1:
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                   "--master-port=29517", *sys.argv])
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2001_04438_b200 as tp
+    from paper_2001_04438_b200 import dist as tpd
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    spec = workload_spec(args.workload, world, rank, args.scaling)
+    rows, cols, dtype = spec["rows"], spec["cols"], spec["dtype"]
+    n_local = rows * cols
+    # inputs: generated on the host (seeded, shard-invariant), pinned, copied once to HBM
+    hx = torch.empty((rows, cols), dtype=torch.float32 if dtype == "f32" else torch.int16, pin_memory=True)
+    hxn = hx.numpy()
+    if dtype == "f32":
+        spec["gen"](hxn)
+    else:
+        hxn[...] = spec["gen"](None).view(np.int16)
+        hx = hx.view(torch.bfloat16)
+    x = hx.to(dev)
+    y = torch.empty((rows, cols), dtype=torch.float32, device=dev)
+    ws = tp.new_workspace(rows, cols, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step_two_pass():
+        if spec["mode"] == "chunk" and world > 1:
+            tpd.chunk_sharded_softmax(x, out=y, workspace=ws)
+        else:
+            tp.softmax_ex(x, tp.ALGO_TWO_PASS, out=y, workspace=ws)
+
+    launches_per_step = 2 if (spec["mode"] == "chunk" and world > 1) else 1
+
+    def timed(step, K, W, sample_clocks=False):
+        for _ in range(W):
+            step()
+        torch.cuda.synchronize(dev)
+        sampler = None
+        if sample_clocks:
+            sampler = ClockSampler(local)
+            sampler.start()
+            t_end = time.time() + args.clock_window_s
+            while time.time() < t_end:
+                step()
+                torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(K):
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        clocks = sampler.stop() if sampler else None
+        total_ms = e0.elapsed_time(e1)
+        per_launch = [a.elapsed_time(b) for a, b in evs]
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), per_launch, clocks
+
+    total_ms, per_launch_ms, clocks = timed(step_two_pass, args.steps, args.warmup, sample_clocks=True)
+    if tp.watchdog_flags(ws, reset=True):
+        raise RuntimeError("watchdog fired during the benchmark: results invalid")
+
+    elems_total = (n_local * world) if spec["scaling"] == "weak" else (
+        workloads_elements(args.workload))
+    per_elem = BYTES_PER_ELEM[("two_pass", dtype)]
+    ms_per_step = total_ms / args.steps
+    value = per_elem * elems_total / (ms_per_step * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    launch_ms = statistics.mean(per_launch_ms)
+    achieved = per_elem * n_local / (launch_ms * 1e-3) / 1e9
+
+    # three-pass comparators, same data, same protocol (not part of the timed region above)
+    three = {}
+    if not args.no_three_pass and not (spec["mode"] == "chunk" and world > 1):
+        for nm, algo in (("recompute", tp.ALGO_RECOMPUTE), ("reload", tp.ALGO_RELOAD)):
+            tot, _, _ = timed(lambda a=algo: tp.softmax_ex(x, a, out=y, workspace=ws), args.steps, args.warmup)
+            ms = tot / args.steps
+            three[nm] = {"ms_per_step": ms,
+                         "GBps_own_cost_model": BYTES_PER_ELEM[(nm, dtype)] * elems_total / (ms * 1e-3) / 1e9,
+                         "GBps_at_two_pass_bytes": value * ms_per_step / ms,
+                         "two_pass_speedup": ms / ms_per_step}
+
+    # end to end through the C ABI on host (pinned) buffers: H2D + kernels + D2H every step
+    e2e = None
+    if not args.no_e2e and (spec["mode"] == "rows" or world == 1):
+        hy = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
+        for _ in range(2):
+            tp.softmax_host(hx, hy)
+        barrier()
+        t0 = time.perf_counter()
+        ke = max(3, min(args.steps, 10))
+        for _ in range(ke):
+            tp.softmax_host(hx, hy)
+        dt = torch.tensor([(time.perf_counter() - t0) / ke], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dt = float(dt.item())
+        e2e = {"value": per_elem * elems_total / dt / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(n_local * (4 if dtype == "f32" else 2)),
+               "d2h_bytes_per_step": int(n_local * 4), "ms_per_step": dt * 1e3, "steps": ke,
+               "api": "softmax_f32_host (C ABI, host buffers)"}
+
+    cpu = cpu_baseline(args, spec) if (rank == 0 and world == 1) else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": spec["scaling"], "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": spec["desc"], "rows_per_rank": rows, "cols": cols,
+                       "elements_total": elems_total, "bytes_per_element": per_elem,
+                       "l2": "inputs larger than L2 (no flush): %.0f MB/rank > 126 MB" %
+                             (n_local * (4 if dtype == 'f32' else 2) / 1e6),
+                       "parallelism": ("rows sharded, no collective" if spec["mode"] == "rows" else
+                                       "row chunk-sharded, one 8-byte (m,n) all_gather per rank")},
+            "elements_per_s": elems_total / (ms_per_step * 1e-3),
+            "pct_of_8TBs": value / world / NOMINAL_HBM_GBS if spec["scaling"] == "weak" else None,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload),
+                         "kernel": "tp::persistent_kernel<float,kTwoPass>" if dtype == "f32" else
+                                   "tp::persistent_kernel<bf16,kTwoPass>",
+                         "algorithmic_bytes_per_launch": per_elem * n_local,
+                         "launch_ms_mean": launch_ms, "peak_source": peak_src},
+            "three_pass": three or None,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * launches_per_step,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def workloads_elements(key):
+    import workloads
+    return workloads.CONFIGS[key].elements
+
+
+if __name__ == "__main__":
+    main()

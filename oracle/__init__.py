@@ -67,6 +67,7 @@ def lib():
             f.restype = i64
         L.oracle_extexp.argtypes = [vp, i64, vp, vp]
         L.oracle_exp_scaled.argtypes = [vp, vp, i64, vp]
+        L.oracle_threads.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -82,6 +83,11 @@ def _kind(x: np.ndarray) -> str:
     if x.dtype == np.uint16:
         return "bf16"  # bf16 bit patterns
     raise TypeError(f"oracle takes float32 or bf16-as-uint16, got {x.dtype}")
+
+
+def threads() -> int:
+    """OpenMP threads the oracle runs on."""
+    return int(lib().oracle_threads())
 
 
 def row_stats(x: np.ndarray) -> tuple[float, np.longdouble]:

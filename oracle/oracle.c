@@ -28,6 +28,13 @@
 
 #define ORACLE_CHUNK 65536
 
+#ifdef _OPENMP
+#include <omp.h>
+int oracle_threads(void) { return omp_get_max_threads(); }
+#else
+int oracle_threads(void) { return 1; }
+#endif
+
 static inline double bf16_value(uint16_t b) {
     union { uint32_t u; float f; } v;
     v.u = (uint32_t)b << 16;

@@ -3,6 +3,8 @@
 // the method lives here; every step runs in the kernels of tp_kernels.cu.
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
+#include <utility>
 
 #include "../../include/twopass.h"
 #include "tp_internal.h"
@@ -49,12 +51,37 @@ int current_device(int* dev) {
     return TP_OK;
 }
 
+// Last (rows, cols) each workspace was launched with.  The kernels leave the control region
+// reusable for the same shape; a different shape moves the tickets and flags, so the control
+// region is zeroed (stream-ordered memset) before the launch.
+std::mutex g_shape_mu;
+std::unordered_map<const void*, std::pair<int64_t, int64_t>> g_ws_shape;
+
+int prepare_ws(void* ws, int64_t rows, int64_t cols, cudaStream_t s) {
+    {
+        std::lock_guard<std::mutex> lk(g_shape_mu);
+        auto it = g_ws_shape.find(ws);
+        if (it != g_ws_shape.end() && it->second == std::make_pair(rows, cols)) return TP_OK;
+        g_ws_shape[ws] = std::make_pair(rows, cols);
+    }
+    cudaError_t e = cudaMemsetAsync(ws, 0, tp::workspace_ctrl_bytes(rows, cols), s);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+void forget_ws(const void* ws) {
+    std::lock_guard<std::mutex> lk(g_shape_mu);
+    g_ws_shape.erase(ws);
+}
+
 // Grow-only zero-filled device buffer.  Growth synchronises the device (documented).
 int ensure_zeroed(void** p, size_t* have, size_t need) {
     if (*have >= need && *p) return TP_OK;
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e);
-    if (*p) cudaFree(*p);
+    if (*p) {
+        cudaFree(*p);
+        forget_ws(*p);
+    }
     *p = nullptr;
     *have = 0;
     e = cudaMalloc(p, need);
@@ -122,6 +149,7 @@ int run_softmax(int algo, int in_dtype, const void* x, float* y, int64_t rows, i
             if (st) return st;
         }
     }
+    if (tp::softmax_needs_workspace(algo, cols, lo) && (st = prepare_ws(ws, rows, cols, s))) return st;
     cudaError_t e = tp::launch_softmax(algo, in_dtype == TP_IN_BF16, x, y, rows, cols, ws, lo, s);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
@@ -138,6 +166,7 @@ int run_partial(int in_dtype, const void* x, int64_t rows, int64_t cols, float* 
         st = internal_workspace(need, &ws);
         if (st) return st;
     }
+    if ((st = prepare_ws(ws, rows, cols, s))) return st;
     cudaError_t e = tp::launch_partial(in_dtype == TP_IN_BF16, x, rows, cols, pair_out, ws, to_opts(opts), s);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
@@ -200,6 +229,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
             if (e != cudaSuccess) return cuda_fail(e);
             cudaEventRecord(d.ev[c], cp);
             cudaStreamWaitEvent(cm, d.ev[c], 0);
+            if ((st = prepare_ws(d.row_ws, 1, cl, cm))) return st;
             e = tp::launch_partial(in_dtype == TP_IN_BF16, dx + (size_t)c * cl * esz, 1, cl, pairs + 2 * c,
                                    d.row_ws, lo, cm);
             if (e != cudaSuccess) return cuda_fail(e);
@@ -248,7 +278,10 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return cuda_fail(e);
             for (int i = 0; i < 2; ++i) {
-                if (d.hws[i]) cudaFree(d.hws[i]);
+                if (d.hws[i]) {
+                    cudaFree(d.hws[i]);
+                    forget_ws(d.hws[i]);
+                }
                 if ((e = cudaMalloc(&d.hws[i], wsb)) != cudaSuccess) return cuda_fail(e);
                 if ((e = cudaMemset(d.hws[i], 0, wsb)) != cudaSuccess) return cuda_fail(e);
             }
@@ -262,6 +295,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         e = cudaMemcpyAsync(d.hx_dev[k], (const char*)hx + (size_t)(r0 * cols) * esz, (size_t)(nr * cols) * esz,
                             cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e);
+        if (needs_ws && (st = prepare_ws(d.hws[k], nr, cols, s))) return st;
         e = tp::launch_softmax(TP_ALGO_TWO_PASS, in_dtype == TP_IN_BF16, d.hx_dev[k], d.hy_dev[k], nr, cols,
                                d.hws[k], lo, s);
         if (e != cudaSuccess) return cuda_fail(e);
@@ -356,6 +390,7 @@ int softmax_watchdog_flags(const void* workspace, int reset) {
     tp::WsHeader h;
     if (cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     if (reset && h.error) {
+        forget_ws(ws);  // the aborted launch may have left tickets behind: re-zero on next use
         unsigned z = 0;
         cudaMemcpy((char*)ws + offsetof(tp::WsHeader, error), &z, sizeof(z), cudaMemcpyHostToDevice);
     }

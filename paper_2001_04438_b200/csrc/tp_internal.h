@@ -18,7 +18,8 @@ struct WsHeader {
 constexpr unsigned long long kWaitTimeoutNs = 4000000000ull;  // 4 s: only a bug can wait this long
 
 struct WsLayout {
-    size_t block_vals, group_vals, group_tickets, row_tickets, row_stats, row_ready, bytes;
+    size_t group_tickets, row_tickets, row_ready, ctrl_bytes;  // control region [0, ctrl_bytes)
+    size_t row_stats, block_vals, group_vals, bytes;           // data region
 };
 
 struct LaunchOpts {
@@ -28,6 +29,9 @@ struct LaunchOpts {
 };
 
 size_t workspace_bytes(int64_t rows, int64_t cols);
+// The control region's layout depends on (rows, cols): it must be re-zeroed whenever a
+// workspace is used with a different shape than its previous launch (tp_api.cu does that).
+size_t workspace_ctrl_bytes(int64_t rows, int64_t cols);
 bool softmax_needs_workspace(int algo, int64_t cols, const LaunchOpts& o);
 cudaError_t launch_softmax(int algo, int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, void* ws,
                            const LaunchOpts& o, cudaStream_t s);

@@ -27,22 +27,26 @@ namespace tp {
 // ----------------------------------------------------------------------------- workspace
 __host__ __device__ inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+// Control region first (header, tickets, row flags: must be zero when a launch starts; the
+// kernels leave it that way except for the epoch-tagged flags), then the data region.
 __host__ __device__ inline WsLayout ws_layout(int64_t rows, int64_t cols) {
     WsLayout L{};
     const int64_t nb = (cols + kBlockElems - 1) / kBlockElems;
     const int64_t ng = (nb + kGroupBlocks - 1) / kGroupBlocks;
     size_t off = align256(sizeof(WsHeader));
-    L.block_vals = off;    off = align256(off + sizeof(float2) * rows * nb);
-    L.group_vals = off;    off = align256(off + sizeof(float2) * rows * ng);
     L.group_tickets = off; off = align256(off + sizeof(unsigned) * rows * ng);
     L.row_tickets = off;   off = align256(off + sizeof(unsigned) * rows);
-    L.row_stats = off;     off = align256(off + sizeof(float4) * rows * 2);
     L.row_ready = off;     off = align256(off + sizeof(unsigned) * rows * 2);
+    L.ctrl_bytes = off;
+    L.row_stats = off;     off = align256(off + sizeof(float4) * rows * 2);
+    L.block_vals = off;    off = align256(off + sizeof(float2) * rows * nb);
+    L.group_vals = off;    off = align256(off + sizeof(float2) * rows * ng);
     L.bytes = off;
     return L;
 }
 
 size_t workspace_bytes(int64_t rows, int64_t cols) { return ws_layout(rows, cols).bytes; }
+size_t workspace_ctrl_bytes(int64_t rows, int64_t cols) { return ws_layout(rows, cols).ctrl_bytes; }
 
 struct KArgs {
     const void* x;
