@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libtwopass.so")
 SOURCES = ["tp_kernels.cu", "tp_api.cu", "tp_debug.cu"]
-HEADERS = ["tp_common.cuh", "tp_io.cuh", "tp_internal.h"]
+HEADERS = ["tp_common.cuh", "tp_block.cuh", "tp_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

@@ -129,6 +129,7 @@ tp::LaunchOpts to_opts(const softmax_opts* o) {
         L.grid_ctas = o->grid_ctas;
         L.lookahead_rows = o->lookahead_rows;
         L.force_persistent = o->force_persistent;
+        L.no_tma = o->disable_tma;
     }
     return L;
 }
@@ -176,7 +177,10 @@ int run_finish(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols
     int st = check_args(in_dtype, x, y, rows, cols, true);
     if (st) return st;
     if (!pairs || world < 1) return TP_EINVAL;
-    cudaError_t e = tp::launch_finish(in_dtype == TP_IN_BF16, x, y, rows, cols, pairs, world, to_opts(opts), s);
+    void* ws = nullptr;
+    if ((st = internal_workspace(tp::workspace_bytes(rows, cols), &ws))) return st;
+    if ((st = prepare_ws(ws, rows, cols, s))) return st;
+    cudaError_t e = tp::launch_finish(in_dtype == TP_IN_BF16, x, y, rows, cols, pairs, world, ws, to_opts(opts), s);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 
@@ -236,7 +240,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         }
         for (int c = 0; c < K; ++c) {  // pass 2 of chunk c || D2H chunk c-1
             e = tp::launch_finish(in_dtype == TP_IN_BF16, dx + (size_t)c * cl * esz, dy + (size_t)c * cl, 1, cl,
-                                  pairs, K, lo, cm);
+                                  pairs, K, d.row_ws, lo, cm);
             if (e != cudaSuccess) return cuda_fail(e);
             cudaEventRecord(d.ev[32 + c], cm);
             cudaStreamWaitEvent(cp, d.ev[32 + c], 0);

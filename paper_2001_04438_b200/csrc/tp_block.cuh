@@ -1,0 +1,192 @@
+// Block-level pieces of the Two-Pass and Three-Pass kernels: per-thread loads (shared-memory
+// stage or global), per-thread pass computations, stores.
+//
+// A block is kBlockElems consecutive elements of one row (reading G8).  Thread t of the CTA
+// owns the vectors j = t + kThreads*k (k = 0..NV-1) of V consecutive elements (V = 4 fp32,
+// 8 bf16): every warp-wide access is a contiguous 512-byte segment.  The per-thread element
+// assignment, and therefore every rounding, is the same whatever the data source (TMA stage,
+// 128-bit global loads, scalar loads of misaligned rows).  A partial last block is masked
+// element by element.
+#pragma once
+#include "tp_common.cuh"
+
+namespace tp {
+
+template <typename In> struct InTraits;
+template <> struct InTraits<float> { static constexpr int V = 4; };
+template <> struct InTraits<uint16_t> { static constexpr int V = 8; };
+
+// This thread's 32 values of a block; v[k*V + q] = element V*(t + kThreads*k) + q.
+struct BlockVals {
+    float v[kPerThread];
+};
+
+template <int V>
+__device__ __forceinline__ int elem_off(int i) {  // i = k*V + q
+    return V * ((int)threadIdx.x + kThreads * (i / V)) + (i % V);
+}
+
+__device__ __forceinline__ void unpack_bf16x8(uint4 a, float* d) {
+    d[0] = bf16_lo(a.x); d[1] = bf16_hi(a.x); d[2] = bf16_lo(a.y); d[3] = bf16_hi(a.y);
+    d[4] = bf16_lo(a.z); d[5] = bf16_hi(a.z); d[6] = bf16_lo(a.w); d[7] = bf16_hi(a.w);
+}
+
+// From a shared-memory stage holding the block (elements past `valid` are stale: callers mask).
+template <typename In>
+__device__ __forceinline__ void load_stage(const In* stage, BlockVals& r) {
+    constexpr int V = InTraits<In>::V, NV = kPerThread / V;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int e = V * ((int)threadIdx.x + kThreads * k);
+        if constexpr (V == 4) {
+            const float4 a = *reinterpret_cast<const float4*>(stage + e);
+            r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
+        } else {
+            unpack_bf16x8(*reinterpret_cast<const uint4*>(stage + e), &r.v[8 * k]);
+        }
+    }
+}
+
+// From global memory.  `vec`: 16-byte aligned rows (128-bit loads); otherwise scalar loads.
+// Elements past `valid` read as 0 (callers mask).  `last` = evict-first L2 policy.
+template <typename In>
+__device__ __forceinline__ void load_global(const In* xb, int valid, bool vec, bool last, BlockVals& r) {
+    constexpr int V = InTraits<In>::V, NV = kPerThread / V;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int e = V * ((int)threadIdx.x + kThreads * k);
+        if (vec && e + V <= valid) {
+            if constexpr (V == 4) {
+                const float4* p = reinterpret_cast<const float4*>(xb + e);
+                const float4 a = last ? __ldcs(p) : __ldg(p);
+                r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
+            } else {
+                const uint4* p = reinterpret_cast<const uint4*>(xb + e);
+                unpack_bf16x8(last ? __ldcs(p) : __ldg(p), &r.v[8 * k]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                float val = 0.0f;
+                if (e + q < valid) {
+                    if constexpr (V == 4) val = __ldg(xb + e + q);
+                    else val = __uint_as_float((uint32_t)__ldg(xb + e + q) << 16);
+                }
+                r.v[k * V + q] = val;
+            }
+        }
+    }
+}
+
+// Coherent loads of fp32 data written earlier in the same kernel (Reload's Y), fp32 layout.
+__device__ __forceinline__ void load_global_y(const float* yb, int valid, bool vec, BlockVals& r) {
+    constexpr int NV = kPerThread / 4;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int e = 4 * ((int)threadIdx.x + kThreads * k);
+        if (vec && e + 4 <= valid) {
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(yb + e));
+            r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r.v[4 * k + q] = (e + q < valid) ? __ldcg(yb + e + q) : 0.0f;
+        }
+    }
+}
+
+// Store this thread's outputs (fp32 for every input dtype), V-element layout of In.
+template <int V>
+__device__ __forceinline__ void store_block(float* yb, int valid, bool vec, const BlockVals& r) {
+    constexpr int NV = kPerThread / V;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int e = V * ((int)threadIdx.x + kThreads * k);
+        if (vec && e + V <= valid) {
+#pragma unroll
+            for (int h = 0; h < V; h += 4)
+                st_cs_f4(yb + e + h, make_float4(r.v[k * V + h], r.v[k * V + h + 1], r.v[k * V + h + 2],
+                                                 r.v[k * V + h + 3]));
+        } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q)
+                if (e + q < valid) yb[e + q] = r.v[k * V + q];
+        }
+    }
+}
+
+// Pass 1 on this thread's values: ExtExp and the pair accumulation
+// in 4 groups of 8 elements.  Masked elements are (m, n) = (0, -inf).
+template <int V, bool FULL, bool CLAMP>
+__device__ __forceinline__ Pair pass1_thread(const BlockVals& r, int valid) {
+    Acc acc = acc_init();
+#pragma unroll
+    for (int g = 0; g < kPerThread / 8; ++g) {
+        float2 m[4], n[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            ext_exp2<CLAMP>(make_float2(r.v[8 * g + 2 * j], r.v[8 * g + 2 * j + 1]), m[j], n[j]);
+            if (!FULL) {
+                const float ninf = -__int_as_float(0x7f800000);
+                if (!(elem_off<V>(8 * g + 2 * j) < valid)) { m[j].x = 0.0f; n[j].x = ninf; }
+                if (!(elem_off<V>(8 * g + 2 * j + 1) < valid)) { m[j].y = 0.0f; n[j].y = ninf; }
+            }
+        }
+        acc_add8(acc, m, n);
+    }
+    return acc_pair(acc);
+}
+
+// Pass 2 in place: y = (m * lambda') * 2^(n - (n_sum - 1)), lambda' = 0.5 / m_sum
+// (PAPER.md:166-168 with reading G9: never form lambda * 2^k first).
+template <bool CLAMP>
+__device__ __forceinline__ void pass2_thread(BlockVals& r, float nsum1, float lam_half) {
+#pragma unroll
+    for (int i = 0; i < kPerThread; i += 2) {
+        float2 m, n;
+        ext_exp2<CLAMP>(make_float2(r.v[i], r.v[i + 1]), m, n);
+        const float2 k = fadd2(n, bc2(-nsum1));
+        const float2 y = fmul2(fmul2(m, bc2(lam_half)), make_float2(ex2_ftz(k.x), ex2_ftz(k.y)));
+        r.v[i] = y.x;
+        r.v[i + 1] = y.y;
+    }
+}
+
+// ---- Three-Pass helpers (Alg. 1/2)
+template <int V, bool FULL>
+__device__ __forceinline__ float max_thread(const BlockVals& r, int valid) {
+    float mx = -__int_as_float(0x7f800000);
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i)
+        if (FULL || elem_off<V>(i) < valid) mx = fmaxf(mx, r.v[i]);
+    return mx;
+}
+
+// e_i = Exp(x_i - mu) in place (Alg. 1 line PAPER.md:93 / Alg. 2), returns the
+// thread's sum in element order (two lanes, then lane x + lane y).
+template <int V, bool FULL>
+__device__ __forceinline__ float exp_sum_thread(BlockVals& r, int valid, float mu) {
+    float2 s = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i < kPerThread; i += 2) {
+        float2 e = exp_flush2(fadd2(make_float2(r.v[i], r.v[i + 1]), bc2(-mu)));
+        if (!FULL) {
+            if (!(elem_off<V>(i) < valid)) e.x = 0.0f;
+            if (!(elem_off<V>(i + 1) < valid)) e.y = 0.0f;
+        }
+        r.v[i] = e.x;
+        r.v[i + 1] = e.y;
+        s = fadd2(s, e);
+    }
+    return __fadd_rn(s.x, s.y);
+}
+
+__device__ __forceinline__ void scale_thread(BlockVals& r, float lam) {
+#pragma unroll
+    for (int i = 0; i < kPerThread; i += 2) {
+        const float2 y = fmul2(bc2(lam), make_float2(r.v[i], r.v[i + 1]));
+        r.v[i] = y.x;
+        r.v[i + 1] = y.y;
+    }
+}
+
+}  // namespace tp

@@ -1,11 +1,12 @@
 // Device building blocks of the Two-Pass softmax (arXiv 2001.04438) for sm_100a.
 //
-//   L0  ext_exp / exp_flush / pow2_flush   PAPER.md:139-149 (§4), Alg. 4 PAPER.md:234-263 (§6.3)
-//   L1  pair_merge, thread accumulate, CTA trees  Alg. 3 PAPER.md:153-170 (§4)
+//   L0  ext_exp2 / exp_flush2 / pow2 (MUFU.EX2)   PAPER.md:139-149 (§4), Alg. 4 PAPER.md:234-263 (§6.3)
+//   L1  pair_merge, vector accumulate, CTA trees   Alg. 3 PAPER.md:153-170 (§4)
 //
 // Readings of the paper taken here are listed in DESIGN.md ("Readings"), ids G1..G25 as in
-// SURVEY.md §8(c).  Everything is IEEE round-to-nearest fp32 with explicit __f*_rn intrinsics,
-// so the arithmetic is fixed by the source and not by compiler contraction choices.
+// SURVEY.md §8(c).  All arithmetic is IEEE round-to-nearest fp32 written with explicit
+// intrinsics / PTX (fma.rn.f32x2 packs two independent lanes into one FFMA2 instruction and is
+// bit-identical to two scalar fma.rn), so results are fixed by the source, not by the compiler.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -19,10 +20,13 @@ constexpr float kLog2e = 0x1.715476p+0f;          // 0x3FB8AA3B
 constexpr float kLn2Hi = 0x1.62e430p-1f;          // RN32(ln 2)            0x3F317218
 constexpr float kLn2Lo = -0x1.05c610p-29f;        // RN32(ln 2 - kLn2Hi)   0xB102E308
 // 1.5 * 2^23: fma(x, log2e, kMagic) - kMagic is round-to-nearest-even of the exact
-// product x*log2e whenever |x*log2e| < 2^22 (guaranteed by the clamp below).
+// product x*log2e whenever |x*log2e| < 2^22.
 constexpr float kMagic = 0x1.8p23f;
-// Guaranteed-accuracy domain |x| <= 2^21 (reading G11); inputs outside are clamped.
+// Guaranteed-accuracy domain |x| <= 2^21 (reading G11).  Blocks whose extended exponent
+// leaves [-kNLimit, kNLimit] (or whose mantissa is not finite) are recomputed with x clamped
+// to [-2^21, 2^21]; inside the domain the clamp is the identity, so both paths agree bit for bit.
 constexpr float kXClamp = 0x1.0p21f;
+constexpr float kNLimit = 3025525.5f;             // > round(2^21 log2 e) = 3025525
 // Degree-5 polynomial p(t) = 1 + t(c1 + t(c2 + t(c3 + t(c4 + t c5)))) for e^t on
 // |t| <= 0.3476.  The paper's Sollya coefficients are not printed
 // (reading G3); these come from tools/fit_exp_poly.py (relative minimax + fp32
@@ -37,8 +41,9 @@ constexpr float kC5 = 0x1.1000a8p-7f;   // 0.00830085948
 // groups of kGroupBlocks blocks.  These, not the grid size, fix every rounding.
 constexpr int kBlockElems = 16384;
 constexpr int kGroupBlocks = 64;
-constexpr int kThreads = 256;                     // one CTA processes one block
-constexpr int kPerThread = kBlockElems / kThreads;  // 64 elements per thread per block
+constexpr int kThreads = 512;                       // one CTA processes one block
+constexpr int kPerThread = kBlockElems / kThreads;  // 32 elements per thread per block
+constexpr float kFltMax = 3.40282347e38f;
 
 struct Pair {
     float m;  // "mantissa" m = e^t, in [sqrt(2)/2, sqrt(2)] for a single element
@@ -47,50 +52,83 @@ struct Pair {
 
 __device__ __forceinline__ Pair pair_identity() { return Pair{0.0f, -__int_as_float(0x7f800000)}; }
 
+// ----------------------------------------------------------------------------- f32x2 (FFMA2 / FADD2 / FMUL2)
+__device__ __forceinline__ unsigned long long pk2(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 upk2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+
 // ----------------------------------------------------------------------------- L0
-// 2^k for integer-valued k <= 1, flushed to +0 for k < -126 (reading G5),
-// and for k = -inf or NaN (identity merges, reading G6): fmaxf drops NaN.
+// 2^k for integer-valued k <= 1 by MUFU.EX2 (exact on integers; pinned by the exhaustive GPU
+// unit test), flushed to +0 below 2^-126 by .ftz (reading G5); 2^-inf = 0.
+__device__ __forceinline__ float ex2_ftz(float k) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(k));
+    return r;
+}
+
+// The same function for the tree merges, NaN-safe: k = NaN (identity + identity) gives 0
+// (reading G6).  Exponent-field construction: fmaxf drops NaN, kc + 127 lands in the low
+// mantissa bits of kc + 1.5*2^23 + 127 and is shifted into the exponent field.
 __device__ __forceinline__ float pow2_flush(float k) {
     const float kc = fmaxf(k, -127.0f);
-    const float b = __fadd_rn(kc, kMagic + 127.0f);  // low mantissa bits hold kc + 127 in [0, 128]
-    return __int_as_float(__float_as_int(b) << 23);   // -> exponent field; kc = -127 -> +0.0
+    const float b = __fadd_rn(kc, kMagic + 127.0f);
+    return __int_as_float(__float_as_int(b) << 23);
 }
 
-// ExtExp: Alg. 4 without the reconstruction step.
+// ExtExp of two elements: Alg. 4 without the reconstruction step.
+template <bool CLAMP>
+__device__ __forceinline__ void ext_exp2(float2 x, float2& m, float2& n) {
+    if (CLAMP) {  // reading G11 (NaN -> -2^21, reading G14)
+        x.x = fminf(fmaxf(x.x, -kXClamp), kXClamp);
+        x.y = fminf(fmaxf(x.y, -kXClamp), kXClamp);
+    }
+    const float2 v = ffma2(x, bc2(kLog2e), bc2(kMagic));
+    n = fadd2(v, bc2(-kMagic));                        // n = round(x log2 e)
+    float2 t = ffma2(n, bc2(-kLn2Hi), x);              // t = x - n ln2, Cody-Waite
+    t = ffma2(n, bc2(-kLn2Lo), t);
+    float2 p = ffma2(bc2(kC5), t, bc2(kC4));           // Horner with FMA
+    p = ffma2(p, t, bc2(kC3));
+    p = ffma2(p, t, bc2(kC2));
+    p = ffma2(p, t, bc2(kC1));
+    m = ffma2(p, t, bc2(1.0f));
+}
+
+// Exp with reconstruction for the Three-Pass comparators (Alg. 4), argument
+// d = x - mu <= 0 (PAPER.md:258 footnote): y = p * s, s = 2^n or 0 below 2^-126 (reading G5).
+__device__ __forceinline__ float2 exp_flush2(float2 d) {
+    d.x = fmaxf(d.x, -kXClamp);
+    d.y = fmaxf(d.y, -kXClamp);
+    float2 m, n;
+    ext_exp2<false>(d, m, n);
+    return fmul2(m, make_float2(ex2_ftz(n.x), ex2_ftz(n.y)));
+}
+
+// Scalar ExtExp (unit-test hook and the rare scalar paths): the same arithmetic as ext_exp2.
 __device__ __forceinline__ Pair ext_exp(float x) {
-    x = fminf(fmaxf(x, -kXClamp), kXClamp);           // reading G11 (NaN -> -2^21, G14)
-    const float v = __fmaf_rn(x, kLog2e, kMagic);
-    const float n = __fsub_rn(v, kMagic);             // n = round(x log2 e)
-    float t = __fmaf_rn(n, -kLn2Hi, x);               // t = x - n ln2, Cody-Waite
-    t = __fmaf_rn(n, -kLn2Lo, t);
-    float p = __fmaf_rn(kC5, t, kC4);                 // Horner with FMA
-    p = __fmaf_rn(p, t, kC3);
-    p = __fmaf_rn(p, t, kC2);
-    p = __fmaf_rn(p, t, kC1);
-    const float m = __fmaf_rn(p, t, 1.0f);
-    return Pair{m, n};
-}
-
-// Exp with reconstruction for the Three-Pass comparators (Alg. 4),
-// argument d = x - mu <= 0 (PAPER.md:258 footnote); s = 2^n or 0 below -126 (reading G5).
-__device__ __forceinline__ float exp_flush(float d) {
-    d = fmaxf(d, -kXClamp);
-    const float v = __fmaf_rn(d, kLog2e, kMagic);
-    const float n = __fsub_rn(v, kMagic);
-    float t = __fmaf_rn(n, -kLn2Hi, d);
-    t = __fmaf_rn(n, -kLn2Lo, t);
-    float p = __fmaf_rn(kC5, t, kC4);
-    p = __fmaf_rn(p, t, kC3);
-    p = __fmaf_rn(p, t, kC2);
-    p = __fmaf_rn(p, t, kC1);
-    p = __fmaf_rn(p, t, 1.0f);
-    return __fmul_rn(p, pow2_flush(n));              // y = p * s
+    float2 m, n;
+    ext_exp2<true>(make_float2(x, x), m, n);
+    return Pair{m.x, n.x};
 }
 
 // ----------------------------------------------------------------------------- L1
 // (m_a, n_a) + (m_b, n_b) with max-exponent rescaling (Alg. 3 update):
-// neither side is ever scaled up.  Both products are exact scalings, so
-// the result is one rounding of the exact sum.  Always called as merge(left, right).
+// neither side is ever scaled up.  Both products are exact scalings, so the
+// result is one rounding of the exact sum.  Always called as merge(left, right).
 __device__ __forceinline__ Pair pair_merge(Pair a, Pair b) {
     const float n = fmaxf(a.n, b.n);
     const float sa = pow2_flush(__fsub_rn(a.n, n));
@@ -98,20 +136,34 @@ __device__ __forceinline__ Pair pair_merge(Pair a, Pair b) {
     return Pair{__fmaf_rn(a.m, sa, __fmul_rn(b.m, sb)), n};
 }
 
-// Accumulate V element pairs into acc, one max and one rescale per vector (Alg. 3 lines
-// PAPER.md:160-162 applied to a vector): n_max over the vector and acc, acc scaled by
-// 2^(n_acc - n_max), then each m_j 2^(n_j - n_max) added in order with one FMA.
-template <int V>
-__device__ __forceinline__ void pair_accumulate(Pair& acc, const float (&m)[V], const float (&n)[V]) {
+// Thread accumulator: two mantissa lanes sharing one exponent (Alg. 3's (m_sum, n_sum),
+// PAPER.md:155-162, kept as two partial sums for FFMA2).  n starts at -FLT_MAX (not -inf) so
+// that n - n_max is never -inf - (-inf); a thread with no element keeps m = 0, which merges
+// like the identity.
+struct Acc {
+    float2 m;
+    float n;
+};
+__device__ __forceinline__ Acc acc_init() { return Acc{make_float2(0.0f, 0.0f), -kFltMax}; }
+
+// Accumulate 8 element pairs (4 float2): one max and one rescale per group of 8, then
+// m_j 2^(n_j - n_max) added with one FFMA2 per two elements (Alg. 3 lines PAPER.md:160-162).
+__device__ __forceinline__ void acc_add8(Acc& acc, const float2 (&m)[4], const float2 (&n)[4]) {
     float nmax = acc.n;
 #pragma unroll
-    for (int j = 0; j < V; ++j) nmax = fmaxf(nmax, n[j]);
-    float s = __fmul_rn(acc.m, pow2_flush(__fsub_rn(acc.n, nmax)));
+    for (int j = 0; j < 4; ++j) nmax = fmaxf(nmax, fmaxf(n[j].x, n[j].y));
+    const float sa = ex2_ftz(__fsub_rn(acc.n, nmax));
+    float2 s = fmul2(acc.m, bc2(sa));
 #pragma unroll
-    for (int j = 0; j < V; ++j) s = __fmaf_rn(m[j], pow2_flush(__fsub_rn(n[j], nmax)), s);
+    for (int j = 0; j < 4; ++j) {
+        const float2 k = fadd2(n[j], bc2(-nmax));
+        s = ffma2(m[j], make_float2(ex2_ftz(k.x), ex2_ftz(k.y)), s);
+    }
     acc.m = s;
     acc.n = nmax;
 }
+
+__device__ __forceinline__ Pair acc_pair(const Acc& a) { return Pair{__fadd_rn(a.m.x, a.m.y), a.n}; }
 
 // ----------------------------------------------------------------------------- CTA trees
 // Perfect binary tree over the CTA's kThreads values in thread order (left = lower index).
@@ -262,6 +314,11 @@ __device__ __forceinline__ float cta_canonical_sum(int64_t n, LeafFn leaf, float
     return cta_tree_sum(v, smem);
 }
 
+// True when the block result needs the clamped recomputation (see kNLimit).
+__device__ __forceinline__ bool pair_out_of_domain(Pair p) {
+    return !(fabsf(p.m) <= kFltMax) || !(fabsf(p.n) <= kNLimit);
+}
+
 // ----------------------------------------------------------------------------- memory ops
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     unsigned v;
@@ -282,5 +339,55 @@ __device__ __forceinline__ void st_cs_f4(float* p, float4 v) { __stcs(reinterpre
 // bf16 bits -> fp32: exact 16-bit left shift
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// ----------------------------------------------------------------------------- TMA bulk copies + mbarriers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// L2 policies for the bulk loads: keep pass-1 data for the re-read, drop last reads first.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// global -> shared bulk copy (TMA, non-tensor), completion counted on the mbarrier
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
 
 }  // namespace tp

@@ -18,14 +18,15 @@ struct WsHeader {
 constexpr unsigned long long kWaitTimeoutNs = 4000000000ull;  // 4 s: only a bug can wait this long
 
 struct WsLayout {
-    size_t group_tickets, row_tickets, row_ready, ctrl_bytes;  // control region [0, ctrl_bytes)
+    size_t group_tickets, row_tickets, row_ready, row_clamp, ctrl_bytes;  // control region [0, ctrl_bytes)
     size_t row_stats, block_vals, group_vals, bytes;           // data region
 };
 
 struct LaunchOpts {
     int64_t grid_ctas = 0;       // 0 = one full wave of resident CTAs
     int64_t lookahead_rows = 0;  // 0 = automatic
-    int force_persistent = 0;    // use the persistent kernel even for single-block rows
+    int force_persistent = 0;    // two-phase schedule even for single-block rows
+    int no_tma = 0;              // global loads instead of TMA staging (testing)
 };
 
 size_t workspace_bytes(int64_t rows, int64_t cols);
@@ -38,7 +39,7 @@ cudaError_t launch_softmax(int algo, int in_bf16, const void* x, float* y, int64
 cudaError_t launch_partial(int in_bf16, const void* x, int64_t rows, int64_t cols, float* pair_out, void* ws,
                            const LaunchOpts& o, cudaStream_t s);
 cudaError_t launch_finish(int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
-                          int world, const LaunchOpts& o, cudaStream_t s);
+                          int world, void* ws, const LaunchOpts& o, cudaStream_t s);
 
 // debug / unit-test kernels (tp_debug.cu)
 cudaError_t launch_debug(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,

@@ -203,6 +203,34 @@ def test_bitwise_deterministic_across_grid_and_lookahead():
         assert np.array_equal(ref, to_host(tp.softmax_ex(xd, grid_ctas=g, lookahead_rows=la))), (g, la)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", [(3, 1000), (2, 16384 * 3 + 8), (1, 16384 * 70)])
+def test_tma_and_global_load_paths_agree_bitwise(rows, cols, dtype):
+    x = workloads.ragged_case(rows, cols, -400, 400, seed=3, stream=cols)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    for algo in ALGOS.values():
+        a = to_host(tp.softmax_ex(xd, algo))
+        b = to_host(tp.softmax_ex(xd, algo, disable_tma=True))
+        assert np.array_equal(a, b), algo
+
+
+def test_out_of_domain_blocks_take_the_clamped_path():
+    # a row with one huge element, a row entirely below -2^21, a row with +-inf/NaN-free extremes:
+    # outputs finite, non-negative, summing to 1; in-domain rows unaffected (reading G11)
+    x = workloads.ragged_case(4, 40000, -50, 50, seed=1, stream=77)
+    x[0, 12345] = 1e30
+    x[1, :] = -5e6
+    x[1, 777] = -4e6
+    x[2, 100] = 3e6
+    y = to_host(tp.softmax(to_dev(x)))
+    assert np.all(np.isfinite(y)) and np.all(y >= 0)
+    assert np.allclose(y.sum(1), 1.0, atol=2e-5)
+    assert y[0, 12345] == 1.0 and y[2, 100] == 1.0
+    assert_parity(x[3:], y[3:], "in-domain row")
+
+
 def test_rowblock_and_persistent_paths_agree_bitwise():
     for cols in [1, 1000, 16384]:
         xd = to_dev(workloads.ragged_case(5, cols, -100, 100, seed=5, stream=cols))
