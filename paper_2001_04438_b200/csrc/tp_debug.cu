@@ -22,7 +22,8 @@ __global__ void debug_kernel(int what, const float* a, const float* b, float* o0
             o1[i] = p.n;
             break;
         }
-        case 3: o0[i] = exp_flush(a[i]); break;
+        case 3: o0[i] = exp_flush2(make_float2(a[i], a[i])).x; break;
+        case 4: o0[i] = ex2_ftz(a[i]); break;
         default: break;
     }
 }

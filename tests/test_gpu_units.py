@@ -81,6 +81,17 @@ def test_pow2_flush_exhaustive():
     assert s[-2] == 0.0 and s[-1] == 0.0                         # identity and NaN (reading G6)
 
 
+def test_mufu_ex2_is_exact_on_integers():
+    # the kernels build 2^(n_i - n_max) with ex2.approx.ftz on integer arguments: it must be the
+    # exact power of two for k >= -126, 0 below (flush, reading G5) and for -inf
+    k = np.concatenate([np.arange(-400, 2, dtype=np.float32), np.float32([-np.inf, -1e30, -3e6])])
+    s, _ = tp.debug_op(4, torch.from_numpy(k).cuda())
+    s = s.cpu().numpy()
+    for ki, si in zip(k, s):
+        want = 0.0 if ki < -126 else math.ldexp(1.0, int(ki))
+        assert si == np.float32(want), (ki, si)
+
+
 def _merge(a, b):
     a = torch.from_numpy(np.asarray(a, np.float32).reshape(-1)).cuda()
     b = torch.from_numpy(np.asarray(b, np.float32).reshape(-1)).cuda()
