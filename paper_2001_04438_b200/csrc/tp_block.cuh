@@ -151,6 +151,77 @@ __device__ __forceinline__ void pass2_thread(BlockVals& r, float nsum1, float la
     }
 }
 
+// ---- warp-level pass 1 with the out-of-domain fallback (reading G11)
+// A lane is out of domain when its accumulator is not finite or its exponent leaves
+// [-kNLimit, kNLimit]; then the whole warp recomputes its 32 x 32 values with x clamped to
+// [-2^21, 2^21].  The clamp is the identity inside the domain, so the choice never changes an
+// in-domain result; pass 2 of the same block applies the same per-warp choice (block mask).
+__device__ __forceinline__ bool acc_out_of_domain(Pair p) {
+    return !(fabsf(p.m) <= kFltMax) || !(fabsf(p.n) <= kNLimit);
+}
+
+// Tree over the 32 lanes of a warp in lane order (left = lower lane); result in lane 0.
+__device__ __forceinline__ Pair warp_tree_pairs(Pair v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        Pair r;
+        r.m = __shfl_down_sync(0xffffffffu, v.m, o);
+        r.n = __shfl_down_sync(0xffffffffu, v.n, o);
+        if ((lane & (2 * o - 1)) == 0) v = pair_merge(v, r);
+    }
+    return v;
+}
+
+__device__ __forceinline__ float warp_tree_sum(float v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float r = __shfl_down_sync(0xffffffffu, v, o);
+        if ((lane & (2 * o - 1)) == 0) v = __fadd_rn(v, r);
+    }
+    return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Perfect tree over the kThreads/32 warp pairs of a block, in warp order.
+constexpr int kWarps = kThreads / 32;
+__device__ __forceinline__ Pair block_tree_warps(const Pair* w) {
+    Pair t[kWarps];
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) t[i] = w[i];
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1)
+#pragma unroll
+        for (int i = 0; i + o < kWarps; i += 2 * o) t[i] = pair_merge(t[i], t[i + o]);
+    return t[0];
+}
+__device__ __forceinline__ float block_tree_warps_sum(const float* w) {
+    float t[kWarps];
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) t[i] = w[i];
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1)
+#pragma unroll
+        for (int i = 0; i + o < kWarps; i += 2 * o) t[i] = __fadd_rn(t[i], t[i + o]);
+    return t[0];
+}
+
+// Pass 1 of this warp's share of a block: warp pair in lane 0, returns the clamp decision.
+template <int V>
+__device__ __forceinline__ bool warp_pass1(const BlockVals& r, int valid, Pair* wp) {
+    Pair acc = valid == kBlockElems ? pass1_thread<V, true, false>(r, valid) : pass1_thread<V, false, false>(r, valid);
+    const bool clamped = __any_sync(0xffffffffu, acc_out_of_domain(acc));
+    if (clamped) acc = pass1_thread<V, false, true>(r, valid);
+    *wp = warp_tree_pairs(acc);
+    return clamped;
+}
+
 // ---- Three-Pass helpers (Alg. 1/2)
 template <int V, bool FULL>
 __device__ __forceinline__ float max_thread(const BlockVals& r, int valid) {

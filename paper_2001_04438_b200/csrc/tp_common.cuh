@@ -369,6 +369,22 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ bool mbar_test_parity(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // L2 policies for the bulk loads: keep pass-1 data for the re-read, drop last reads first.
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;

@@ -1,0 +1,144 @@
+// Per-item operations shared by the warp-specialised TMA kernel (tp_stream.cu) and the general
+// kernel (tp_kernels.cu), so both compute bit-identical results.
+//
+// Compute side (every compute warp, on its 32 x 32 values of the block):
+//   op_pass1        Alg. 3 pass 1: warp pair + clamp decision -> part[w]
+//   op_pass2        Alg. 3 pass 2 -> y
+//   op_fused_tail   rows of one block: block pair from part[], lambda, pass 2 -> y
+//   op_max / op_expsum / op_out_*   Three-Pass passes
+// Retire side (one warp): the block value from part[], publication and row finishing.
+#pragma once
+#include "tp_sched.cuh"
+
+namespace tp {
+
+struct Part {
+    Pair v[kWarps];           // per-warp pair (Two-Pass) or value in .m (max / sum)
+    unsigned char cb[kWarps]; // per-warp clamp decision of pass 1
+};
+
+template <int V>
+__device__ __forceinline__ void op_pass1(const BlockVals& r, int valid, Part& part) {
+    Pair wp;
+    const bool cl = warp_pass1<V>(r, valid, &wp);
+    if ((threadIdx.x & 31) == 0) {
+        part.v[threadIdx.x >> 5] = wp;
+        part.cb[threadIdx.x >> 5] = cl ? 1 : 0;
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void op_pass2(BlockVals& r, float4 st, bool clamp, float* yb, int valid, bool vec) {
+    if (clamp) pass2_thread<true>(r, st.x, st.y);
+    else pass2_thread<false>(r, st.x, st.y);
+    store_block<V>(yb, valid, vec, r);
+}
+
+// After every compute warp has run op_pass1 and a barrier among them: the row pair is the
+// block pair (one block per row), lambda' and pass 2 on the same staged values.
+template <int V>
+__device__ __forceinline__ void op_fused_tail(BlockVals& r, const Part& part, float* yb, int valid, bool vec) {
+    const Pair root = block_tree_warps(part.v);
+    const float4 st = make_float4(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m), 0.0f, 0.0f);
+    op_pass2<V>(r, st, part.cb[threadIdx.x >> 5] != 0, yb, valid, vec);
+}
+
+template <int V>
+__device__ __forceinline__ void op_max(const BlockVals& r, int valid, Part& part) {
+    const float m = warp_max(valid == kBlockElems ? max_thread<V, true>(r, valid) : max_thread<V, false>(r, valid));
+    if ((threadIdx.x & 31) == 0) part.v[threadIdx.x >> 5] = Pair{m, 0.0f};
+}
+
+template <int V, bool RELOAD>
+__device__ __forceinline__ void op_expsum(BlockVals& r, int valid, float mu, Part& part, float* yb, bool vec) {
+    float s = valid == kBlockElems ? exp_sum_thread<V, true>(r, valid, mu) : exp_sum_thread<V, false>(r, valid, mu);
+    if (RELOAD) store_block<V>(yb, valid, vec, r);  // Y_i <- Exp(X_i - mu)
+    s = warp_tree_sum(s);
+    if ((threadIdx.x & 31) == 0) part.v[threadIdx.x >> 5] = Pair{s, 0.0f};
+}
+
+template <int V>
+__device__ __forceinline__ void op_out_recompute(BlockVals& r, float4 st, float* yb, int valid, bool vec) {
+    exp_sum_thread<V, false>(r, valid, st.x);
+    scale_thread(r, st.y);  // Y_i <- lambda * Exp(X_i - mu)
+    store_block<V>(yb, valid, vec, r);
+}
+
+__device__ __forceinline__ void op_out_reload(float4 st, float* yb, int valid, bool yvec) {
+    BlockVals r;
+    load_global_y(yb, valid, yvec, r);
+    scale_thread(r, st.y);  // Y_i <- lambda * Y_i
+    store_block<4>(yb, valid, yvec, r);
+}
+
+// Retire a phase's block (one whole warp): block value from the warp parts, its clamp mask
+// (Two-Pass pass 1), publication, and the row's statistics / partial pair when this block
+// completed the row.
+template <int A>
+__device__ __forceinline__ void retire_block(const KArgs& a, const Item& it, const Part& part, unsigned want,
+                                             float mu) {
+    const int lane = threadIdx.x & 31;
+    const int kind = red_kind<A>(it.phase);
+    float2 val = make_float2(0.0f, 0.0f);
+    if (lane == 0) {
+        if (kind == kRedPair) {
+            const Pair bp = block_tree_warps(part.v);
+            unsigned mask = 0;
+            for (int w = 0; w < kWarps; ++w) mask |= (unsigned)part.cb[w] << w;
+            reinterpret_cast<unsigned*>(a.ws + a.lay.block_clamp)[it.row * a.nb + it.blk] = mask;
+            val = make_float2(bp.m, bp.n);
+        } else if (kind == kRedMax) {
+            float m = part.v[0].m;
+            for (int w = 1; w < kWarps; ++w) m = fmaxf(m, part.v[w].m);
+            val = make_float2(m, 0.0f);
+        } else {
+            float s[kWarps];
+            for (int w = 0; w < kWarps; ++w) s[w] = part.v[w].m;
+            val = make_float2(block_tree_warps_sum(s), 0.0f);
+        }
+    }
+    float2 root;
+    if (publish_warp<A>(a, it.phase, it.row, it.blk, val, &root) && lane == 0) {
+        if (A == kPartial) {
+            a.pair_out[it.row] = root;
+        } else {
+            float4* row_stats = reinterpret_cast<float4*>(a.ws + a.lay.row_stats);
+            unsigned* row_ready = reinterpret_cast<unsigned*>(a.ws + a.lay.row_ready);
+            row_stats[it.row * 2 + it.phase] = row_stats_of<A>(it.phase, root, mu);
+            st_release_gpu(row_ready + it.row * 2 + it.phase, want);
+        }
+    }
+}
+
+// Statistics a later-phase item needs: (stats, per-warp clamp mask).  Called by one thread
+// after the row's previous phase has been released.
+template <int A>
+__device__ __forceinline__ void item_stats(const KArgs& a, const Item& it, float4* st, unsigned* mask) {
+    const float4* row_stats = reinterpret_cast<const float4*>(a.ws + a.lay.row_stats);
+    *st = __ldcg(row_stats + it.row * 2 + (it.phase - 1));
+    *mask = 0;
+    if (A == kTwoPass) *mask = __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) + it.row * a.nb + it.blk);
+}
+
+// kFinish: merge the world partials of a row with the canonical tree over rank index.
+__device__ __forceinline__ float4 finish_stats(const KArgs& a, int64_t row) {
+    const Pair root = seq_tree_pairs((int)next_pow2(a.world), [&](int i) {
+        if (i >= a.world) return pair_identity();
+        const float2 v = a.pairs_in[(int64_t)i * a.rows + row];
+        return Pair{v.x, v.y};
+    });
+    return make_float4(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m), 0.0f, 0.0f);
+}
+
+template <int A>
+__device__ __forceinline__ bool item_needs_stats(const Item& it) {
+    return (AlgoTraits<A>::P > 1 && it.phase > 0) || A == kFinish;
+}
+
+// host side (tp_kernels.cu / tp_stream.cu)
+int device_sms(int dev);
+int64_t lookahead_rows(const KArgs& a, int64_t grid, int items_per_cta, const LaunchOpts& o);
+template <typename In, int A>
+cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s);
+
+}  // namespace tp
