@@ -15,6 +15,8 @@
 // Deadlock freedom: items are handed out in increasing order, a CTA works through its items in
 // that order, and an item depends only on items of smaller index; so the smallest unfinished
 // item is always the current item of a running CTA.
+#include <cstdlib>
+
 #include "tp_ops.cuh"
 
 namespace tp {
@@ -139,7 +141,7 @@ static int vec_ok(const void* x, const float* y, int64_t cols) {
 int64_t lookahead_rows(const KArgs& a, int64_t grid, int items_per_cta, const LaunchOpts& o) {
     // enough rows that a row's pass-1 items are done before its pass-2 items are handed out
     // (about two grids of items in flight)
-    int64_t L = o.lookahead_rows > 0 ? o.lookahead_rows : (2 * grid * items_per_cta + a.nb - 1) / a.nb + 1;
+    int64_t L = o.lookahead_rows > 0 ? o.lookahead_rows : (grid * items_per_cta + a.nb - 1) / a.nb + 2;
     if (L < 1) L = 1;
     if (L > a.rows) L = a.rows;
     return L;
@@ -180,6 +182,11 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
     a.pairs_in = pairs_in;
     a.world = world;
     a.vec = vec_ok<In>(x, y, cols);
+    static const int hints = [] {
+        const char* e = getenv("TP_L2_HINTS");
+        return e ? atoi(e) : 1;
+    }();
+    a.l2_hints = hints;
     if (a.vec && !o.no_tma) return launch_stream<In, A>(a, o, s);
     return launch_general<In, A>(a, o, s);
 }

@@ -57,6 +57,7 @@ struct KArgs {
     const float2* pairs_in;  // kFinish: world x rows pairs, rank-major
     int world;
     int vec;                 // 16-byte aligned rows
+    int l2_hints;            // TMA loads carry evict_last / evict_first L2 policies
 };
 
 // number of (phase, row) units in schedule slots < s

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
     __shared__ unsigned s_epoch;
+    __shared__ Part ctrl_part;  // control warp's copy of a retiring block's warp values
 
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -110,8 +111,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 const bool keep = (P > 1 && it.phase < P - 1) || A == kPartial;
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(&full_bar[s], bytes);
-                tma_load_1d(stages + (size_t)s * kBlockElems, x + it.row * a.cols + e0, bytes, &full_bar[s],
-                            keep ? pol_keep : pol_drop);
+                if (a.l2_hints)
+                    tma_load_1d(stages + (size_t)s * kBlockElems, x + it.row * a.cols + e0, bytes, &full_bar[s],
+                                keep ? pol_keep : pol_drop);
+                else
+                    tma_load_1d_nohint(stages + (size_t)s * kBlockElems, x + it.row * a.cols + e0, bytes,
+                                       &full_bar[s]);
             }
             if (!need) mbar_arrive(&full_bar[s]);
         };
@@ -168,16 +173,24 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 while (!mbar_test_parity(&empty_bar[s], parity)) try_provide();
             }
             __syncwarp();
+            // snapshot what retiring needs, refill the stage first, then retire (the retire's
+            // fence + ticket atomic overlap the refill's TMA latency)
             const Item it = meta[s].it;
+            const float mu = meta[s].stats.x;
             const bool retire = ((A == kTwoPass || A == kPartial) && it.phase == 0) ||
                                 ((A == kRecompute || A == kReload) && it.phase < 2);
-            if (retire) retire_block<A>(a, it, meta[s].part, want, meta[s].stats.x);
+            if (retire && lane < kWarps) {
+                ctrl_part.v[lane] = meta[s].part.v[lane];
+                ctrl_part.cb[lane] = meta[s].part.cb[lane];
+            }
             __syncwarp();
             if (lane == 0) {
                 issue(j + S);
                 ++issued;
                 try_provide();
             }
+            __syncwarp();
+            if (retire) retire_block<A>(a, it, ctrl_part, want, mu);
             __syncwarp();
         }
         if (lane == 0) exit_and_reset(hdr);

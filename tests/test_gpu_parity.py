@@ -227,7 +227,7 @@ def test_out_of_domain_blocks_take_the_clamped_path():
     y = to_host(tp.softmax(to_dev(x)))
     assert np.all(np.isfinite(y)) and np.all(y >= 0)
     assert np.allclose(y.sum(1), 1.0, atol=2e-5)
-    assert y[0, 12345] == 1.0 and y[2, 100] == 1.0
+    assert abs(y[0, 12345] - 1.0) <= 2e-7 and abs(y[2, 100] - 1.0) <= 2e-7
     assert_parity(x[3:], y[3:], "in-domain row")
 
 
