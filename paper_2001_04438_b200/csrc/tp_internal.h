@@ -18,7 +18,7 @@ struct WsHeader {
 constexpr unsigned long long kWaitTimeoutNs = 4000000000ull;  // 4 s: only a bug can wait this long
 
 struct WsLayout {
-    size_t group_tickets, row_tickets, row_ready, ctrl_bytes;  // control region [0, ctrl_bytes)
+    size_t group_tickets, row_tickets, row_ready, row_clamp, ctrl_bytes;  // control region [0, ctrl_bytes)
     size_t row_stats, block_vals, block_clamp, group_vals, bytes;  // data region
 };
 

@@ -71,53 +71,121 @@ __device__ __forceinline__ void op_out_reload(float4 st, float* yb, int valid, b
     store_block<4>(yb, valid, yvec, r);
 }
 
-// Retire a phase's block (one whole warp): block value from the warp parts, its clamp mask
-// (Two-Pass pass 1), publication, and the row's statistics / partial pair when this block
-// completed the row.
+// Does finishing this item publish a block value?  (Two-Pass pass 1; Three-Pass passes 1-2)
 template <int A>
-__device__ __forceinline__ void retire_block(const KArgs& a, const Item& it, const Part& part, unsigned want,
-                                             float mu) {
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ bool item_retires(const Item& it) {
+    return ((A == kTwoPass || A == kPartial) && it.phase == 0) || ((A == kRecompute || A == kReload) && it.phase < 2);
+}
+
+// The block's value from its warp values (one thread): the pair tree (plus the block's clamp
+// mask, stored for pass 2 and flagged on the row), the max, or the sum tree.
+template <int A>
+__device__ __forceinline__ float2 block_value(const KArgs& a, const Item& it, const Part& part) {
     const int kind = red_kind<A>(it.phase);
-    float2 val = make_float2(0.0f, 0.0f);
-    if (lane == 0) {
-        if (kind == kRedPair) {
-            const Pair bp = block_tree_warps(part.v);
-            unsigned mask = 0;
-            for (int w = 0; w < kWarps; ++w) mask |= (unsigned)part.cb[w] << w;
+    if (kind == kRedPair) {
+        const Pair bp = block_tree_warps(part.v);
+        unsigned mask = 0;
+        for (int w = 0; w < kWarps; ++w) mask |= (unsigned)part.cb[w] << w;
+        if (mask) {
             reinterpret_cast<unsigned*>(a.ws + a.lay.block_clamp)[it.row * a.nb + it.blk] = mask;
-            val = make_float2(bp.m, bp.n);
-        } else if (kind == kRedMax) {
-            float m = part.v[0].m;
-            for (int w = 1; w < kWarps; ++w) m = fmaxf(m, part.v[w].m);
-            val = make_float2(m, 0.0f);
-        } else {
-            float s[kWarps];
-            for (int w = 0; w < kWarps; ++w) s[w] = part.v[w].m;
-            val = make_float2(block_tree_warps_sum(s), 0.0f);
+            atomicOr(reinterpret_cast<unsigned*>(a.ws + a.lay.row_clamp) + it.row, 1u);
         }
+        return make_float2(bp.m, bp.n);
     }
-    float2 root;
-    if (publish_warp<A>(a, it.phase, it.row, it.blk, val, &root) && lane == 0) {
-        if (A == kPartial) {
-            a.pair_out[it.row] = root;
-        } else {
-            float4* row_stats = reinterpret_cast<float4*>(a.ws + a.lay.row_stats);
-            unsigned* row_ready = reinterpret_cast<unsigned*>(a.ws + a.lay.row_ready);
-            row_stats[it.row * 2 + it.phase] = row_stats_of<A>(it.phase, root, mu);
-            st_release_gpu(row_ready + it.row * 2 + it.phase, want);
+    if (kind == kRedMax) {
+        float m = part.v[0].m;
+        for (int w = 1; w < kWarps; ++w) m = fmaxf(m, part.v[w].m);
+        return make_float2(m, 0.0f);
+    }
+    float s[kWarps];
+    for (int w = 0; w < kWarps; ++w) s[w] = part.v[w].m;
+    return make_float2(block_tree_warps_sum(s), 0.0f);
+}
+
+// Publish a batch of block values (one whole warp; each lane with `mine` holds one item's
+// value): every lane stores its value, ONE fence covers the batch, every lane takes its group
+// ticket; then each group completed by the batch is reduced by the warp (canonical tree), and
+// a row completed by that group is reduced and released.
+template <int A>
+__device__ void retire_batch(const KArgs& a, bool mine, const Item& it, float2 val, float mu, unsigned want) {
+    const int lane = threadIdx.x & 31;
+    float2* block_vals = reinterpret_cast<float2*>(a.ws + a.lay.block_vals);
+    float2* group_vals = reinterpret_cast<float2*>(a.ws + a.lay.group_vals);
+    unsigned* gt = reinterpret_cast<unsigned*>(a.ws + a.lay.group_tickets);
+    unsigned* rt = reinterpret_cast<unsigned*>(a.ws + a.lay.row_tickets);
+    unsigned* row_clamp = reinterpret_cast<unsigned*>(a.ws + a.lay.row_clamp);
+    const int64_t g = it.blk / kGroupBlocks;
+    if (mine) block_vals[it.row * a.nb + it.blk] = val;
+    __threadfence();
+    bool last = false;
+    if (mine) {
+        const int64_t gsize = min((int64_t)kGroupBlocks, a.nb - g * kGroupBlocks);
+        last = atomicAdd(&gt[it.row * a.ng + g], 1u) == (unsigned)(gsize - 1);
+    }
+    unsigned fin = __ballot_sync(0xffffffffu, last);
+    if (!fin) return;
+    __threadfence();
+    while (fin) {
+        const int l = __ffs(fin) - 1;
+        fin &= fin - 1;
+        const int phase = __shfl_sync(0xffffffffu, it.phase, l);
+        const int64_t row = __shfl_sync(0xffffffffu, it.row, l);
+        const int64_t gg = __shfl_sync(0xffffffffu, g, l);
+        const float mu_l = __shfl_sync(0xffffffffu, mu, l);
+        const int kind = red_kind<A>(phase);
+        const int64_t gsize = min((int64_t)kGroupBlocks, a.nb - gg * kGroupBlocks);
+        const float2* gv = block_vals + row * a.nb + gg * kGroupBlocks;
+        const float2 gres = warp_reduce_leaves(kind, gsize, [&](int64_t j) { return __ldcg(gv + j); });
+        unsigned rlast = 0;
+        if (lane == 0) {
+            gt[row * a.ng + gg] = 0u;  // ticket reset for the next phase / launch
+            group_vals[row * a.ng + gg] = gres;
+            __threadfence();
+            rlast = atomicAdd(&rt[row], 1u) == (unsigned)(a.ng - 1);
+        }
+        if (!__shfl_sync(0xffffffffu, rlast, 0)) continue;
+        __threadfence();
+        const float2* rv = group_vals + row * a.ng;
+        const float2 root = warp_reduce_leaves(kind, a.ng, [&](int64_t j) { return __ldcg(rv + j); });
+        if (lane == 0) {
+            rt[row] = 0u;
+            float clamped = 0.0f;  // did any block of the row take the clamped path?
+            if (A == kTwoPass || A == kPartial) {
+                clamped = __ldcg(&row_clamp[row]) ? 1.0f : 0.0f;
+                row_clamp[row] = 0u;
+            }
+            if (A == kPartial) {
+                a.pair_out[row] = root;
+            } else {
+                float4 st = row_stats_of<A>(phase, root, mu_l);
+                if (A == kTwoPass) st.z = clamped;
+                reinterpret_cast<float4*>(a.ws + a.lay.row_stats)[row * 2 + phase] = st;
+                st_release_gpu(reinterpret_cast<unsigned*>(a.ws + a.lay.row_ready) + row * 2 + phase, want);
+            }
         }
     }
 }
 
+// Retire a phase's block (one whole warp, value from lane 0's view of the warp parts).
+template <int A>
+__device__ __forceinline__ void retire_block(const KArgs& a, const Item& it, const Part& part, unsigned want,
+                                             float mu) {
+    const int lane = threadIdx.x & 31;
+    float2 val = make_float2(0.0f, 0.0f);
+    if (lane == 0) val = block_value<A>(a, it, part);
+    retire_batch<A>(a, lane == 0, it, val, mu, want);
+}
+
 // Statistics a later-phase item needs: (stats, per-warp clamp mask).  Called by one thread
-// after the row's previous phase has been released.
+// after the row's previous phase has been released.  The per-block mask is read only when
+// some block of the row took the clamped path (stats.z, rare).
 template <int A>
 __device__ __forceinline__ void item_stats(const KArgs& a, const Item& it, float4* st, unsigned* mask) {
     const float4* row_stats = reinterpret_cast<const float4*>(a.ws + a.lay.row_stats);
     *st = __ldcg(row_stats + it.row * 2 + (it.phase - 1));
     *mask = 0;
-    if (A == kTwoPass) *mask = __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) + it.row * a.nb + it.blk);
+    if (A == kTwoPass && st->z != 0.0f)
+        *mask = __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) + it.row * a.nb + it.blk);
 }
 
 // kFinish: merge the world partials of a row with the canonical tree over rank index.

@@ -29,6 +29,7 @@ __host__ __device__ inline WsLayout ws_layout(int64_t rows, int64_t cols) {
     L.group_tickets = off; off = align256(off + sizeof(unsigned) * rows * ng);
     L.row_tickets = off;   off = align256(off + sizeof(unsigned) * rows);
     L.row_ready = off;     off = align256(off + sizeof(unsigned) * rows * 2);
+    L.row_clamp = off;     off = align256(off + sizeof(unsigned) * rows);
     L.ctrl_bytes = off;
     L.row_stats = off;     off = align256(off + sizeof(float4) * rows * 2);
     L.block_vals = off;    off = align256(off + sizeof(float2) * rows * nb);
@@ -60,12 +61,14 @@ struct KArgs {
     int l2_hints;            // TMA loads carry evict_last / evict_first L2 policies
 };
 
-// number of (phase, row) units in schedule slots < s
-__device__ __forceinline__ int64_t units_before(int64_t s, int64_t R, int64_t L, int P) {
-    int64_t c = 0;
+// number of (phase, row) units in schedule slots < s.  Item arithmetic is 32-bit: a launch
+// has far fewer than 2^32 items (2^32 blocks would be 2^46 elements).
+__device__ __forceinline__ uint32_t units_before(uint32_t s, uint32_t R, uint32_t L, int P) {
+    uint32_t c = 0;
     for (int p = 0; p < P; ++p) {
-        const int64_t v = s - p * L;
-        c += v < 0 ? 0 : (v > R ? R : v);
+        const uint32_t off = (uint32_t)p * L;
+        const uint32_t v = s > off ? s - off : 0u;
+        c += v > R ? R : v;
     }
     return c;
 }
@@ -76,27 +79,28 @@ struct Item {
 };
 
 template <int A>
-__device__ __forceinline__ Item decode_item(int64_t item, int64_t R, int64_t nb, int64_t L) {
+__device__ __forceinline__ Item decode_item(int64_t item64, int64_t R64, int64_t nb64, int64_t L64) {
     constexpr int P = AlgoTraits<A>::P;
+    const uint32_t item = (uint32_t)item64, R = (uint32_t)R64, nb = (uint32_t)nb64, L = (uint32_t)L64;
     Item it;
-    const int64_t unit = item / nb;
-    const int64_t bi = item - unit * nb;
+    const uint32_t unit = item / nb;
+    const uint32_t bi = item - unit * nb;
     if (P == 1) {
         it.phase = 0;
         it.row = unit;
         it.blk = (A == kFinish) ? nb - 1 - bi : bi;  // pass 2 walks backwards (L2 tail first)
         return it;
     }
-    int64_t lo = 0, hi = R + (P - 1) * L;  // slot s with units_before(s) <= unit < units_before(s+1)
+    uint32_t lo = 0, hi = R + (uint32_t)(P - 1) * L;  // slot s: units_before(s) <= unit < units_before(s+1)
     while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
+        const uint32_t mid = (lo + hi) >> 1;
         if (units_before(mid, R, L, P) <= unit) lo = mid; else hi = mid;
     }
-    const int64_t s = lo;
-    const int p_hi = (int)((s / L) < (P - 1) ? (s / L) : (P - 1));
-    const int64_t idx = unit - units_before(s, R, L, P);
+    const uint32_t s = lo;
+    const int p_hi = (int)((s / L) < (uint32_t)(P - 1) ? (s / L) : (uint32_t)(P - 1));
+    const uint32_t idx = unit - units_before(s, R, L, P);
     it.phase = p_hi - (int)idx;  // within a slot: oldest row (highest phase) first
-    it.row = s - it.phase * L;
+    it.row = s - (uint32_t)it.phase * L;
     it.blk = it.phase > 0 ? nb - 1 - bi : bi;
     return it;
 }

@@ -1,31 +1,38 @@
 // Warp-specialised persistent kernel for 16-byte aligned rows (the fast path of every entry
-// point).  One CTA per SM: 16 compute warps + 1 control warp, and a ring of S shared-memory
-// stages, each holding one block (16384 elements; 3 x 64 KB fp32, 6 x 32 KB bf16).
+// point).  One CTA per SM, three roles:
 //
-// Control warp (lane 0 unless noted):
-//   * takes items from the in-order work queue and starts a cp.async.bulk (TMA) copy of each
-//     item's block into a free stage, S items ahead of the compute warps, with an L2 policy
-//     (evict_last for data that pass 2 will re-read, evict_first for last reads);
-//   * provides later-phase items with their row statistics once the row's previous phase is
-//     released (polled, never blocking, while it waits for stages to drain);
-//   * retires finished pass-1 blocks: block value from the 16 warp values, the block's clamp
-//     mask, publication and the group / row reductions (whole warp, tp_sched.cuh).
-// Compute warps: wait for a stage (mbarrier: TMA bytes + the control warp's arrivals), run the
-// item's operation on their 32 x 32 values (tp_ops.cuh), store outputs with 128-bit evict-first
-// stores, release the stage.  They never wait on global atomics or fences.
+//   16 compute warps   wait for a stage, copy their 32 x 32 values into registers and release
+//                      the stage at once, run the item's operation (tp_ops.cuh), store outputs
+//                      with 128-bit evict-first stores, and hand their per-warp results to the
+//                      retire warp through a ring of part slots.  They never touch a global
+//                      atomic or fence.
+//   producer warp      takes items from the in-order work queue (chunks of 2, the next chunk's
+//                      atomic in flight), starts a cp.async.bulk (TMA) copy of each item's block
+//                      into a free stage with an L2 policy (evict_last for data pass 2 will
+//                      re-read, evict_first for last reads), and supplies later-phase items with
+//                      their row statistics as soon as the row's previous phase is released
+//                      (polled, never blocking).
+//   retire warp        publishes finished blocks in batches (one value per lane, one fence per
+//                      batch) and runs the group / row reductions they complete (tp_ops.cuh).
 //
-// Stage protocol per stage s (use count u = seq / S, parity u & 1):
-//   full[s]  count 2: (1) control arrive.expect_tx at issue, (2) control arrive when the item's
-//            statistics are in place (immediately for items that need none); + TMA bytes
-//   empty[s] count 16: one arrive per compute warp when done with the stage
-// Deadlock freedom: as in tp_kernels.cu; in addition the control warp never blocks on a row
-// flag (it polls while waiting for stages), so a CTA can always retire its oldest item.
+// Ring of S stages, each holding one block (16384 elements; 3 x 64 KB fp32, 6 x 32 KB bf16):
+//   full[s]   count 2: producer arrive.expect_tx at issue + producer arrive once the item's
+//             statistics are in place (immediately for items that need none); + TMA bytes
+//   empty[s]  count 16: each compute warp once its values are in registers
+// Ring of R part slots (per item sequence number):
+//   pfull[r]  count 16: each compute warp after writing its part
+//   pempty[r] count 1: the retire warp after reading the slot
+// Deadlock freedom: as in tp_kernels.cu.  In addition no role blocks on a row flag: the
+// producer polls them while it waits for stages, and the retire warp never waits on anything
+// but part slots, so a CTA always retires its oldest finished item.
 #include "tp_ops.cuh"
 
 namespace tp {
 
-constexpr int kCtrlWarp = kWarps;
-constexpr int kStreamThreads = kThreads + 32;
+constexpr int kProducerWarp = kWarps;
+constexpr int kRetireWarp = kWarps + 1;
+constexpr int kStreamThreads = kThreads + 64;
+constexpr int kPartSlots = 8;
 
 template <typename In> struct Ring { static constexpr int S = 3; };   // 3 x 64 KB fp32
 template <> struct Ring<uint16_t> { static constexpr int S = 6; };     // 6 x 32 KB bf16
@@ -37,52 +44,77 @@ struct StageMeta {
     int need;       // statistics still to be provided
     unsigned mask;  // pass 2: per-warp clamp decisions of pass 1
     float4 stats;
+};
+
+struct PartSlot {
+    long long item;
+    Item it;
+    float mu;
     Part part;
 };
 
 template <typename In, int A>
-__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a) {
+__global__ void __maxnreg__(112) stream_kernel(const KArgs a) {  // 576 threads, 1 CTA per SM
     constexpr int P = AlgoTraits<A>::P;
     constexpr int V = InTraits<In>::V;
     constexpr int S = Ring<In>::S;
+    constexpr int R = kPartSlots;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ StageMeta meta[S];
+    __shared__ PartSlot pslot[R];
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
+    __shared__ __align__(8) uint64_t pfull_bar[R];
+    __shared__ __align__(8) uint64_t pempty_bar[R];
     __shared__ unsigned s_epoch;
-    __shared__ Part ctrl_part;  // control warp's copy of a retiring block's warp values
 
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     In* stages = reinterpret_cast<In*>(dsm);
+    const long long total = a.total_items;
 
-    if (threadIdx.x == kCtrlWarp * 32) {
+    if (threadIdx.x == kProducerWarp * 32) {
         s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full_bar[s], 2);
             mbar_init(&empty_bar[s], kWarps);
+        }
+        for (int r = 0; r < R; ++r) {
+            mbar_init(&pfull_bar[r], kWarps);
+            mbar_init(&pempty_bar[r], 1);
         }
         fence_mbar_init();
     }
     __syncthreads();
     const unsigned want = s_epoch + 1u;
 
-    if (warp == kCtrlWarp) {
-        // =============================================================== control warp
+    if (warp == kProducerWarp) {
+        // =============================================================== producer warp
+        if (lane != 0) return;
         const unsigned* row_ready = reinterpret_cast<const unsigned*>(a.ws + a.lay.row_ready);
         const In* x = static_cast<const In*>(a.x);
-        uint64_t pol_keep = 0, pol_drop = 0;
+        const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+        constexpr unsigned long long kChunk = 2;
+        unsigned long long next = atomicAdd(&hdr->counter, kChunk), end = next + kChunk;
+        unsigned long long ahead = atomicAdd(&hdr->counter, kChunk);  // result used one chunk later
         long long issued = 0, prov = 0;
         int64_t cached_row = -1;
         int cached_phase = -1;
         float4 cached_st = make_float4(0.f, 0.f, 0.f, 0.f);
         unsigned long long wait_t0 = 0;
 
-        auto issue = [&](long long seq) {  // lane 0
-            const int s = (int)(seq % S);
-            const long long item = (long long)atomicAdd(&hdr->counter, 1ull);
+        auto take = [&]() -> long long {
+            if (next == end) {
+                next = ahead;
+                end = next + kChunk;
+                ahead = atomicAdd(&hdr->counter, kChunk);
+            }
+            return (long long)next++;
+        };
+
+        auto issue = [&](int s, long long item) {
             meta[s].item = item;
-            if (item >= a.total_items) {  // sentinel: release the compute warps
+            if (item >= total) {  // sentinel: release the compute warps
                 meta[s].need = 0;
                 mbar_arrive(&full_bar[s]);
                 mbar_arrive(&full_bar[s]);
@@ -109,30 +141,26 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             } else {
                 const uint32_t bytes = (uint32_t)valid * (uint32_t)sizeof(In);
                 const bool keep = (P > 1 && it.phase < P - 1) || A == kPartial;
+                In* dst = stages + (size_t)s * kBlockElems;
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(&full_bar[s], bytes);
-                if (a.l2_hints)
-                    tma_load_1d(stages + (size_t)s * kBlockElems, x + it.row * a.cols + e0, bytes, &full_bar[s],
-                                keep ? pol_keep : pol_drop);
-                else
-                    tma_load_1d_nohint(stages + (size_t)s * kBlockElems, x + it.row * a.cols + e0, bytes,
-                                       &full_bar[s]);
+                if (a.l2_hints) tma_load_1d(dst, x + it.row * a.cols + e0, bytes, &full_bar[s], keep ? pol_keep : pol_drop);
+                else tma_load_1d_nohint(dst, x + it.row * a.cols + e0, bytes, &full_bar[s]);
             }
             if (!need) mbar_arrive(&full_bar[s]);
         };
 
-        // statistics for issued items, in order, as far as their rows are released (lane 0)
+        // statistics for issued items, in order, as far as their rows are released
         auto try_provide = [&]() {
             while (prov < issued) {
                 const int s = (int)(prov % S);
-                if (meta[s].item >= a.total_items || !meta[s].need) {
+                if (meta[s].item >= total || !meta[s].need) {
                     ++prov;
                     continue;
                 }
                 const Item it = meta[s].it;
                 if (!(it.row == cached_row && it.phase - 1 == cached_phase)) {
-                    const unsigned* f = row_ready + it.row * 2 + (it.phase - 1);
-                    if (ld_acquire_gpu(f) != want) {
+                    if (ld_acquire_gpu(row_ready + it.row * 2 + (it.phase - 1)) != want) {
                         const unsigned long long now = globaltimer_ns();
                         if (wait_t0 == 0) wait_t0 = now;
                         if (now - wait_t0 <= kWaitTimeoutNs) return;
@@ -147,7 +175,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 }
                 wait_t0 = 0;
                 meta[s].stats = cached_st;
-                meta[s].mask = (A == kTwoPass)
+                meta[s].mask = (A == kTwoPass && cached_st.z != 0.0f)
                                    ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) +
                                             it.row * a.nb + it.blk)
                                    : 0u;
@@ -156,75 +184,99 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             }
         };
 
-        if (lane == 0) {
-            pol_keep = policy_evict_last();
-            pol_drop = policy_evict_first();
-            for (long long q = 0; q < S; ++q) issue(q);
-            issued = S;
-            try_provide();
-        }
-        __syncwarp();
-        for (long long j = 0;; ++j) {
-            const int s = (int)(j % S);
-            const long long item = meta[s].item;  // written by lane 0 before the last __syncwarp
-            if (item >= a.total_items) break;
-            if (lane == 0) {
-                const uint32_t parity = (uint32_t)((j / S) & 1);
+        for (long long seq = 0;; ++seq) {
+            const int s = (int)(seq % S);
+            if (seq >= S) {
+                const uint32_t parity = (uint32_t)(((seq / S) - 1) & 1);
                 while (!mbar_test_parity(&empty_bar[s], parity)) try_provide();
             }
-            __syncwarp();
-            // snapshot what retiring needs, refill the stage first, then retire (the retire's
-            // fence + ticket atomic overlap the refill's TMA latency)
-            const Item it = meta[s].it;
-            const float mu = meta[s].stats.x;
-            const bool retire = ((A == kTwoPass || A == kPartial) && it.phase == 0) ||
-                                ((A == kRecompute || A == kReload) && it.phase < 2);
-            if (retire && lane < kWarps) {
-                ctrl_part.v[lane] = meta[s].part.v[lane];
-                ctrl_part.cb[lane] = meta[s].part.cb[lane];
-            }
-            __syncwarp();
-            if (lane == 0) {
-                issue(j + S);
-                ++issued;
-                try_provide();
-            }
-            __syncwarp();
-            if (retire) retire_block<A>(a, it, ctrl_part, want, mu);
-            __syncwarp();
+            const long long item = take();
+            issue(s, item);
+            ++issued;
+            try_provide();
+            if (item >= total) break;
         }
-        if (lane == 0) exit_and_reset(hdr);
+        while (prov < issued) try_provide();
+        if (ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
+        exit_and_reset(hdr);
+    } else if (warp == kRetireWarp) {
+        // =============================================================== retire warp
+        for (long long seq = 0;;) {
+            int n = 0;
+            if (lane == 0) {
+                mbar_wait_parity(&pfull_bar[seq % R], (uint32_t)((seq / R) & 1));
+                n = 1;
+                while (n < R && mbar_test_parity(&pfull_bar[(seq + n) % R], (uint32_t)(((seq + n) / R) & 1))) ++n;
+            }
+            n = __shfl_sync(0xffffffffu, n, 0);
+            const bool have = lane < n;
+            const PartSlot* ps = &pslot[(seq + lane) % R];
+            const long long item = have ? ps->item : total;
+            const unsigned stop = __ballot_sync(0xffffffffu, have && item >= total);
+            const int m = stop ? __ffs(stop) - 1 : n;  // items before the sentinel
+            Item it{0, 0, 0};
+            float2 val = make_float2(0.f, 0.f);
+            float mu = 0.f;
+            bool mine = false;
+            if (lane < m) {
+                it = ps->it;
+                mu = ps->mu;
+                mine = item_retires<A>(it);
+                if (mine) val = block_value<A>(a, it, ps->part);
+            }
+            retire_batch<A>(a, mine, it, val, mu, want);
+            __syncwarp();
+            if (lane < m) mbar_arrive(&pempty_bar[(seq + lane) % R]);
+            seq += m;
+            if (stop) break;
+        }
     } else {
         // =============================================================== compute warps
         for (long long j = 0;; ++j) {
             const int s = (int)(j % S);
+            const int r = (int)(j % R);
             mbar_wait_parity(&full_bar[s], (uint32_t)((j / S) & 1));
-            if (meta[s].item >= a.total_items) break;
+            if (j >= R) mbar_wait_parity(&pempty_bar[r], (uint32_t)(((j / R) - 1) & 1));
+            PartSlot& ps = pslot[r];
+            const long long item = meta[s].item;
+            if (item >= total) {  // pass the sentinel on to the retire warp
+                if (warp == 0 && lane == 0) ps.item = item;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pfull_bar[r]);
+                break;
+            }
             const Item it = meta[s].it;
             const int valid = meta[s].valid;
             const float4 st = meta[s].stats;
             const bool my_clamp = ((meta[s].mask >> warp) & 1u) != 0;
             float* yb = a.y ? a.y + it.row * a.cols + it.blk * kBlockElems : nullptr;
-            BlockVals r;
-            if (!(A == kReload && it.phase == 2)) load_stage<In>(stages + (size_t)s * kBlockElems, r);
+            BlockVals v;
+            if (!(A == kReload && it.phase == 2)) load_stage<In>(stages + (size_t)s * kBlockElems, v);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[s]);  // the stage is free: values are in registers
 
             if constexpr (A == kFused) {
-                op_pass1<V>(r, valid, meta[s].part);
+                op_pass1<V>(v, valid, ps.part);
                 asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");  // compute warps only
-                op_fused_tail<V>(r, meta[s].part, yb, valid, true);
+                op_fused_tail<V>(v, ps.part, yb, valid, true);
             } else if constexpr (A == kTwoPass || A == kPartial) {
-                if (it.phase == 0) op_pass1<V>(r, valid, meta[s].part);
-                else op_pass2<V>(r, st, my_clamp, yb, valid, true);
+                if (it.phase == 0) op_pass1<V>(v, valid, ps.part);
+                else op_pass2<V>(v, st, my_clamp, yb, valid, true);
             } else if constexpr (A == kFinish) {
-                op_pass2<V>(r, st, true, yb, valid, true);
+                op_pass2<V>(v, st, true, yb, valid, true);
             } else {
-                if (it.phase == 0) op_max<V>(r, valid, meta[s].part);
-                else if (it.phase == 1) op_expsum<V, A == kReload>(r, valid, st.x, meta[s].part, yb, true);
-                else if (A == kRecompute) op_out_recompute<V>(r, st, yb, valid, true);
+                if (it.phase == 0) op_max<V>(v, valid, ps.part);
+                else if (it.phase == 1) op_expsum<V, A == kReload>(v, valid, st.x, ps.part, yb, true);
+                else if (A == kRecompute) op_out_recompute<V>(v, st, yb, valid, true);
                 else op_out_reload(st, yb, valid, true);
             }
+            if (warp == 0 && lane == 0) {
+                ps.item = item;
+                ps.it = it;
+                ps.mu = st.x;
+            }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[s]);
+            if (lane == 0) mbar_arrive(&pfull_bar[r]);
         }
     }
 }

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--algo", default="two_pass")
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--rows", type=int, default=None)
+    ap.add_argument("--no-tma", action="store_true")
+    ap.add_argument("--lookahead", type=int, default=0)
     args = ap.parse_args()
     x = workloads.generate(args.config, nrows=args.rows)
     if x.dtype == np.uint16:
@@ -33,7 +35,7 @@ def main():
         xd = torch.from_numpy(x).cuda()
     y = torch.empty(xd.shape, dtype=torch.float32, device="cuda")
     for _ in range(args.iters):
-        tp.softmax_ex(xd, ALGO[args.algo], out=y)
+        tp.softmax_ex(xd, ALGO[args.algo], out=y, disable_tma=args.no_tma, lookahead_rows=args.lookahead)
     torch.cuda.synchronize()
     assert tp.watchdog_flags() == 0
     assert bool(torch.isfinite(y).all())
