@@ -54,7 +54,8 @@ struct PartSlot {
 };
 
 template <typename In, int A>
-__global__ void __maxnreg__(112) stream_kernel(const KArgs a) {  // 576 threads, 1 CTA per SM
+// 18 warps: 5 on some SM sub-partitions, whose 16K-register files then allow 96 per thread.
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a) {
     constexpr int P = AlgoTraits<A>::P;
     constexpr int V = InTraits<In>::V;
     constexpr int S = Ring<In>::S;
