@@ -298,7 +298,9 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     if (grid > resident) grid = resident;
     if (grid > a.total_items) grid = a.total_items;
     if (grid < 1) grid = 1;
-    a.L = lookahead_rows(a, grid, Ring<In>::S, o);
+    // items a CTA holds between hand-out and retirement: its stages, the prefetched queue chunks
+    // and the part-slot backlog (measured: C4 gains up to L ~ 50 rows, tools/sweep.py)
+    a.L = lookahead_rows(a, grid, Ring<In>::S + 12, o);
     kern<<<(unsigned)grid, kStreamThreads, dyn, s>>>(a);
     return cudaGetLastError();
 }
