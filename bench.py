@@ -367,8 +367,8 @@ def main():
             "pct_of_8TBs": value / world / NOMINAL_HBM_GBS if spec["scaling"] == "weak" else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload),
-                         "kernel": "tp::persistent_kernel<float,kTwoPass>" if dtype == "f32" else
-                                   "tp::persistent_kernel<bf16,kTwoPass>",
+                         "kernel": "tp::stream_kernel<float,kTwoPass>" if dtype == "f32" else
+                                   "tp::stream_kernel<uint16_t,kTwoPass>",
                          "algorithmic_bytes_per_launch": per_elem * n_local,
                          "launch_ms_mean": launch_ms, "peak_source": peak_src},
             "three_pass": three or None,
