@@ -56,6 +56,11 @@ def chunk_sharded_softmax(x_chunk: torch.Tensor, out: torch.Tensor | None = None
                           workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Softmax of rows sharded by column chunk: partial -> all_gather(8 B/row/rank) -> finish."""
     import paper_2001_04438_b200 as tp
+    rows = x_chunk.shape[0]
+    if x_chunk.shape[-1] == 0:  # an empty trailing chunk contributes the identity (0, -inf)
+        pairs = torch.tensor([[0.0, float("-inf")]] * rows, dtype=torch.float32, device=x_chunk.device)
+        exchange_pairs(pairs, group)
+        return torch.empty(x_chunk.shape, dtype=torch.float32, device=x_chunk.device) if out is None else out
     pairs = tp.partial(x_chunk, workspace=workspace)
     allp = exchange_pairs(pairs, group)
     return tp.finish(x_chunk, allp, allp.shape[0], out=out)

@@ -1,0 +1,32 @@
+"""Per-kernel share of an ncu launch list (--metrics gpu__time_duration.sum ... --csv --log-file).
+
+    python tools/launch_share.py profiles/r01_launches_bench_c4.csv
+"""
+import collections
+import csv
+import sys
+
+
+def main(path):
+    lines = [ln for ln in open(path) if ln.startswith('"')]
+    rows = list(csv.reader(lines))
+    h = rows[0]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    per = collections.defaultdict(dict)
+    for r in rows[1:]:
+        per[int(r[ii])][r[mi]] = float(r[vi].replace(",", ""))
+        per[int(r[ii])]["k"] = r[ki]
+    tot, cnt, by = collections.Counter(), collections.Counter(), collections.Counter()
+    for d in per.values():
+        k = d["k"].split("(")[0][:70]
+        tot[k] += d.get("gpu__time_duration.sum", 0)
+        cnt[k] += 1
+        by[k] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+    T = sum(tot.values())
+    for k, t in tot.most_common():
+        print(f"{k:72s} n={cnt[k]:4d} share={t / T:6.1%} mean_us={t / cnt[k] / 1e3:9.1f} "
+              f"dram_MB_per_launch={by[k] / cnt[k] / 1e6:9.1f}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
