@@ -47,9 +47,10 @@ def chunk_range(cols: int, world: int, rank: int) -> tuple[int, int]:
 def exchange_pairs(local_pairs: torch.Tensor, group=None) -> torch.Tensor:
     """all_gather of every rank's [rows, 2] pairs -> [world, rows, 2], rank-major (one collective)."""
     world = dist.get_world_size(group)
-    out = torch.empty((world,) + tuple(local_pairs.shape), dtype=local_pairs.dtype, device=local_pairs.device)
+    rows = local_pairs.shape[0]
+    out = torch.empty((world * rows, 2), dtype=local_pairs.dtype, device=local_pairs.device)
     dist.all_gather_into_tensor(out, local_pairs.contiguous(), group=group)
-    return out
+    return out.view(world, rows, 2)
 
 
 def chunk_sharded_softmax(x_chunk: torch.Tensor, out: torch.Tensor | None = None, group=None,

@@ -67,7 +67,7 @@ def test_pair_exchange_gloo_world2():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in range(world))
+    res = dict(q.get(timeout=60) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
