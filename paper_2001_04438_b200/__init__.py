@@ -41,7 +41,8 @@ class TwoPassError(RuntimeError):
 
 class SoftmaxOpts(ctypes.Structure):
     _fields_ = [("grid_ctas", ctypes.c_int64), ("lookahead_rows", ctypes.c_int64),
-                ("force_persistent", ctypes.c_int), ("disable_tma", ctypes.c_int)]
+                ("force_persistent", ctypes.c_int), ("disable_tma", ctypes.c_int),
+                ("disable_hold", ctypes.c_int)]
 
 
 _lib = None
@@ -112,15 +113,18 @@ def _prep(x: torch.Tensor) -> torch.Tensor:
     return x if x.is_contiguous() else x.contiguous()
 
 
-def _opts(grid_ctas: int = 0, lookahead_rows: int = 0, force_persistent: bool = False, disable_tma: bool = False):
-    if not (grid_ctas or lookahead_rows or force_persistent or disable_tma):
+def _opts(grid_ctas: int = 0, lookahead_rows: int = 0, force_persistent: bool = False, disable_tma: bool = False,
+          disable_hold: bool = False):
+    if not (grid_ctas or lookahead_rows or force_persistent or disable_tma or disable_hold):
         return None
-    return ctypes.pointer(SoftmaxOpts(grid_ctas, lookahead_rows, int(force_persistent), int(disable_tma)))
+    return ctypes.pointer(SoftmaxOpts(grid_ctas, lookahead_rows, int(force_persistent), int(disable_tma),
+                                      int(disable_hold)))
 
 
 def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | None = None,
                workspace: torch.Tensor | None = None, grid_ctas: int = 0, lookahead_rows: int = 0,
-               force_persistent: bool = False, disable_tma: bool = False) -> torch.Tensor:
+               force_persistent: bool = False, disable_tma: bool = False,
+               disable_hold: bool = False) -> torch.Tensor:
     """Row-wise softmax over the last dim; fp32 output.  See include/twopass.h."""
     x = _prep(x)
     rows, cols = _rows_cols(x)
@@ -129,7 +133,8 @@ def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | N
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel() *
                                                              workspace.element_size())
     st = lib().softmax_ex(algo, _in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, ws_ptr, ws_bytes,
-                          _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma), _stream())
+                          _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma, disable_hold),
+                          _stream())
     _check(st, "softmax")
     return y
 

@@ -59,6 +59,7 @@ struct KArgs {
     int world;
     int vec;                 // 16-byte aligned rows
     int l2_hints;            // TMA loads carry evict_last / evict_first L2 policies
+    int hold;                // stream kernel: blocks stay staged between pass 1 and pass 2
 };
 
 // number of (phase, row) units in schedule slots < s.  Item arithmetic is 32-bit: a launch

@@ -1,30 +1,33 @@
 // Warp-specialised persistent kernel for 16-byte aligned rows (the fast path of every entry
 // point).  One CTA per SM, three roles:
 //
-//   16 compute warps   wait for a stage, copy their 32 x 32 values into registers and release
-//                      the stage at once, run the item's operation (tp_ops.cuh), store outputs
-//                      with 128-bit evict-first stores, and hand their per-warp results to the
-//                      retire warp through a ring of part slots.  They never touch a global
-//                      atomic or fence.
+//   16 compute warps   execute commands from the producer in order.  A command names a stage
+//                      and an operation (tp_ops.cuh) on the block in it; the warps copy their
+//                      32 x 32 values into registers, compute, store outputs with 128-bit
+//                      evict-first stores and hand per-warp results to the retire warp through
+//                      a ring of part slots.  They never touch a global atomic or fence.
 //   producer warp      takes items from the in-order work queue (chunks of 2, the next chunk's
 //                      atomic in flight), starts a cp.async.bulk (TMA) copy of each item's block
-//                      into a free stage with an L2 policy (evict_last for data pass 2 will
-//                      re-read, evict_first for last reads), and supplies later-phase items with
-//                      their row statistics as soon as the row's previous phase is released
-//                      (polled, never blocking).
+//                      into a free stage, polls the row flags its items depend on (never
+//                      blocking), and pushes commands as their inputs become available.
 //   retire warp        publishes finished blocks in batches (one value per lane, one fence per
 //                      batch) and runs the group / row reductions they complete (tp_ops.cuh).
 //
-// Ring of S stages, each holding one block (16384 elements; 3 x 64 KB fp32, 6 x 32 KB bf16):
-//   full[s]   count 2: producer arrive.expect_tx at issue + producer arrive once the item's
-//             statistics are in place (immediately for items that need none); + TMA bytes
-//   empty[s]  count 16: each compute warp once its values are in registers
-// Ring of R part slots (per item sequence number):
-//   pfull[r]  count 16: each compute warp after writing its part
-//   pempty[r] count 1: the retire warp after reading the slot
-// Deadlock freedom: as in tp_kernels.cu.  In addition no role blocks on a row flag: the
-// producer polls them while it waits for stages, and the retire warp never waits on anything
-// but part slots, so a CTA always retires its oldest finished item.
+// Two schedules:
+//   hold    (Two-Pass, rows of 2..hold_max blocks): an item is one block; the block stays in
+//           its stage between pass 1 (command P1) and pass 2 (command P2, pushed once the row's
+//           pass 1 is released), so pass 2 re-reads it from shared memory, not from L2/HBM.
+//   stream  (single-block rows, rows too long to hold, partial/finish, Three-Pass): an item is
+//           one phase of one block (tp_sched.cuh decode_item); its stage is released as soon as
+//           the values are in registers.
+//
+// Barriers: full[s] (count 1 + TMA bytes), empty[s] (count 16, one per compute warp when it is
+// done reading the stage), cmd_full[c] (count 1) / cmd_empty[c] (count 16) for the command ring,
+// pfull[r] (count 16) / pempty[r] (count 1) for the part ring.
+// Deadlock freedom: items are handed out in increasing order; a command is pushed only when
+// its inputs exist (no compute warp ever waits for a row); no role blocks on a row flag; so the
+// smallest unfinished item always progresses.  In hold mode a row must fit in the CTAs' stages
+// many times over (hold_max = grid * S / 4 blocks), so the oldest held row is always complete.
 #include "tp_ops.cuh"
 
 namespace tp {
@@ -33,17 +36,25 @@ constexpr int kProducerWarp = kWarps;
 constexpr int kRetireWarp = kWarps + 1;
 constexpr int kStreamThreads = kThreads + 64;
 constexpr int kPartSlots = 8;
+constexpr int kCmdSlots = 16;
 
 template <typename In> struct Ring { static constexpr int S = 3; };   // 3 x 64 KB fp32
 template <> struct Ring<uint16_t> { static constexpr int S = 6; };     // 6 x 32 KB bf16
+
+enum CmdOp : int { kOpItem = 0, kOpP1 = 1, kOpP2 = 2, kOpExit = 3 };
 
 struct StageMeta {
     long long item;
     Item it;
     int valid;
-    int need;       // statistics still to be provided
     unsigned mask;  // pass 2: per-warp clamp decisions of pass 1
     float4 stats;
+};
+
+struct Cmd {
+    int op;
+    int stage;
+    unsigned parity;  // full[stage] parity of this use
 };
 
 struct PartSlot {
@@ -53,18 +64,22 @@ struct PartSlot {
     Part part;
 };
 
-template <typename In, int A>
 // 18 warps: 5 on some SM sub-partitions, whose 16K-register files then allow 96 per thread.
+template <typename In, int A>
 __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a) {
     constexpr int P = AlgoTraits<A>::P;
     constexpr int V = InTraits<In>::V;
     constexpr int S = Ring<In>::S;
     constexpr int R = kPartSlots;
+    constexpr int C = kCmdSlots;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ StageMeta meta[S];
     __shared__ PartSlot pslot[R];
+    __shared__ Cmd cmds[C];
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
+    __shared__ __align__(8) uint64_t cfull_bar[C];
+    __shared__ __align__(8) uint64_t cempty_bar[C];
     __shared__ __align__(8) uint64_t pfull_bar[R];
     __shared__ __align__(8) uint64_t pempty_bar[R];
     __shared__ unsigned s_epoch;
@@ -73,12 +88,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     In* stages = reinterpret_cast<In*>(dsm);
     const long long total = a.total_items;
+    const bool hold = a.hold != 0;
 
     if (threadIdx.x == kProducerWarp * 32) {
         s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full_bar[s], 2);
+            mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], kWarps);
+        }
+        for (int c = 0; c < C; ++c) {
+            mbar_init(&cfull_bar[c], 1);
+            mbar_init(&cempty_bar[c], kWarps);
         }
         for (int r = 0; r < R; ++r) {
             mbar_init(&pfull_bar[r], kWarps);
@@ -98,7 +118,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         constexpr unsigned long long kChunk = 2;
         unsigned long long next = atomicAdd(&hdr->counter, kChunk), end = next + kChunk;
         unsigned long long ahead = atomicAdd(&hdr->counter, kChunk);  // result used one chunk later
-        long long issued = 0, prov = 0;
+        bool exhausted = false;
+        long long pushed = 0;
+        unsigned use[S];       // issues of each stage so far
+        int state[S];          // 0 free, 1 busy (until its empty barrier completes), 2 waiting for stats
+        long long order[S];    // issue sequence of the stage's item (stats are provided in this order)
+        for (int s = 0; s < S; ++s) use[s] = 0, state[s] = 0, order[s] = 0;
+        long long issue_seq = 0;
         int64_t cached_row = -1;
         int cached_phase = -1;
         float4 cached_st = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -113,20 +139,81 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             return (long long)next++;
         };
 
-        auto issue = [&](int s, long long item) {
-            meta[s].item = item;
-            if (item >= total) {  // sentinel: release the compute warps
-                meta[s].need = 0;
-                mbar_arrive(&full_bar[s]);
-                mbar_arrive(&full_bar[s]);
-                return;
+        auto push = [&](int op, int s, unsigned parity) {
+            const int c = (int)(pushed % C);
+            if (pushed >= C) mbar_wait_parity(&cempty_bar[c], (uint32_t)(((pushed / C) - 1) & 1));
+            cmds[c] = Cmd{op, s, parity};
+            mbar_arrive(&cfull_bar[c]);
+            ++pushed;
+        };
+
+        // statistics of the row phase an item depends on, if released (cached per row)
+        auto stats_ready = [&](const Item& it, int dep_phase, float4* st) -> bool {
+            if (!(it.row == cached_row && dep_phase == cached_phase)) {
+                if (ld_acquire_gpu(row_ready + it.row * 2 + dep_phase) != want) {
+                    const unsigned long long now = globaltimer_ns();
+                    if (wait_t0 == 0) wait_t0 = now;
+                    if (now - wait_t0 <= kWaitTimeoutNs) return false;
+                    atomicOr(&hdr->error, 1u);  // never hang the GPU on a bug
+                }
+                cached_st = __ldcg(reinterpret_cast<const float4*>(a.ws + a.lay.row_stats) + it.row * 2 + dep_phase);
+                cached_row = it.row;
+                cached_phase = dep_phase;
             }
-            const Item it = decode_item<A>(item, a.rows, a.nb, a.L);
+            wait_t0 = 0;
+            *st = cached_st;
+            return true;
+        };
+
+        // push the commands whose statistics are now available, oldest item first
+        auto poll = [&]() {
+            for (;;) {
+                int best = -1;
+                for (int s = 0; s < S; ++s)
+                    if (state[s] == 2 && (best < 0 || order[s] < order[best])) best = s;
+                if (best < 0) return;
+                const Item it = meta[best].it;
+                float4 st;
+                if (!stats_ready(it, hold ? 0 : it.phase - 1, &st)) return;
+                meta[best].stats = st;
+                meta[best].mask = (A == kTwoPass && st.z != 0.0f)
+                                      ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) +
+                                               it.row * a.nb + it.blk)
+                                      : 0u;
+                state[best] = 1;
+                push(hold ? kOpP2 : kOpItem, best, (use[best] - 1) & 1u);
+            }
+        };
+
+        auto issue = [&](int s, long long item) {
+            Item it;
+            if (hold) {  // one item per block: (row, blk), pass 1 then pass 2 on the same stage
+                const uint32_t u = (uint32_t)item, nb = (uint32_t)a.nb;
+                it.phase = 0;
+                it.row = u / nb;
+                it.blk = u - (u / nb) * nb;
+            } else {
+                it = decode_item<A>(item, a.rows, a.nb, a.L);
+            }
             const int64_t e0 = it.blk * kBlockElems;
             const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
+            meta[s].item = item;
             meta[s].it = it;
             meta[s].valid = valid;
-            bool need = item_needs_stats<A>(it);
+            const unsigned parity = use[s] & 1u;
+            ++use[s];
+            order[s] = issue_seq++;
+            if (A == kReload && it.phase == 2) {  // Reload's pass 3 reads Y, not X: no copy
+                mbar_arrive(&full_bar[s]);
+            } else {
+                const uint32_t bytes = (uint32_t)valid * (uint32_t)sizeof(In);
+                const bool keep = !hold && ((P > 1 && it.phase < P - 1) || A == kPartial);
+                In* dst = stages + (size_t)s * kBlockElems;
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&full_bar[s], bytes);
+                if (a.l2_hints) tma_load_1d(dst, x + it.row * a.cols + e0, bytes, &full_bar[s], keep ? pol_keep : pol_drop);
+                else tma_load_1d_nohint(dst, x + it.row * a.cols + e0, bytes, &full_bar[s]);
+            }
             if (A == kFinish) {
                 if (it.row != cached_row) {
                     cached_st = finish_stats(a, it.row);
@@ -134,70 +221,34 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 }
                 meta[s].stats = cached_st;
                 meta[s].mask = 0xffffffffu;  // the chunk's pass-1 clamp decisions are not known here
-                need = false;
             }
-            meta[s].need = need ? 1 : 0;
-            if (A == kReload && it.phase == 2) {  // Reload's pass 3 reads Y, not X: no copy
-                mbar_arrive(&full_bar[s]);
+            if (hold) {
+                state[s] = 2;  // P1 now, P2 once the row is released
+                push(kOpP1, s, parity);
+            } else if (item_needs_stats<A>(it) && A != kFinish) {
+                state[s] = 2;
+                poll();
             } else {
-                const uint32_t bytes = (uint32_t)valid * (uint32_t)sizeof(In);
-                const bool keep = (P > 1 && it.phase < P - 1) || A == kPartial;
-                In* dst = stages + (size_t)s * kBlockElems;
-                fence_proxy_async_smem();
-                mbar_arrive_expect_tx(&full_bar[s], bytes);
-                if (a.l2_hints) tma_load_1d(dst, x + it.row * a.cols + e0, bytes, &full_bar[s], keep ? pol_keep : pol_drop);
-                else tma_load_1d_nohint(dst, x + it.row * a.cols + e0, bytes, &full_bar[s]);
-            }
-            if (!need) mbar_arrive(&full_bar[s]);
-        };
-
-        // statistics for issued items, in order, as far as their rows are released
-        auto try_provide = [&]() {
-            while (prov < issued) {
-                const int s = (int)(prov % S);
-                if (meta[s].item >= total || !meta[s].need) {
-                    ++prov;
-                    continue;
-                }
-                const Item it = meta[s].it;
-                if (!(it.row == cached_row && it.phase - 1 == cached_phase)) {
-                    if (ld_acquire_gpu(row_ready + it.row * 2 + (it.phase - 1)) != want) {
-                        const unsigned long long now = globaltimer_ns();
-                        if (wait_t0 == 0) wait_t0 = now;
-                        if (now - wait_t0 <= kWaitTimeoutNs) return;
-                        atomicOr(&hdr->error, 1u);  // never hang the GPU on a bug
-                    }
-                    float4 st;
-                    unsigned mk;
-                    item_stats<A>(a, it, &st, &mk);
-                    cached_st = st;
-                    cached_row = it.row;
-                    cached_phase = it.phase - 1;
-                }
-                wait_t0 = 0;
-                meta[s].stats = cached_st;
-                meta[s].mask = (A == kTwoPass && cached_st.z != 0.0f)
-                                   ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) +
-                                            it.row * a.nb + it.blk)
-                                   : 0u;
-                mbar_arrive(&full_bar[s]);
-                ++prov;
+                state[s] = 1;
+                push(kOpItem, s, parity);
             }
         };
 
-        for (long long seq = 0;; ++seq) {
-            const int s = (int)(seq % S);
-            if (seq >= S) {
-                const uint32_t parity = (uint32_t)(((seq / S) - 1) & 1);
-                while (!mbar_test_parity(&empty_bar[s], parity)) try_provide();
+        for (;;) {
+            poll();
+            bool busy = false;
+            for (int s = 0; s < S; ++s) {
+                if (state[s] == 1 && mbar_test_parity(&empty_bar[s], (use[s] - 1) & 1u)) state[s] = 0;
+                if (state[s] == 0 && !exhausted) {
+                    const long long item = take();
+                    if (item >= total) exhausted = true;
+                    else issue(s, item);
+                }
+                busy |= state[s] != 0;
             }
-            const long long item = take();
-            issue(s, item);
-            ++issued;
-            try_provide();
-            if (item >= total) break;
+            if (exhausted && !busy) break;
         }
-        while (prov < issued) try_provide();
+        push(kOpExit, 0, 0);
         if (ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
         exit_and_reset(hdr);
     } else if (warp == kRetireWarp) {
@@ -214,7 +265,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             const PartSlot* ps = &pslot[(seq + lane) % R];
             const long long item = have ? ps->item : total;
             const unsigned stop = __ballot_sync(0xffffffffu, have && item >= total);
-            const int m = stop ? __ffs(stop) - 1 : n;  // items before the sentinel
+            const int m = stop ? __ffs(stop) - 1 : n;  // slots before the sentinel
             Item it{0, 0, 0};
             float2 val = make_float2(0.f, 0.f);
             float mu = 0.f;
@@ -233,19 +284,36 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         }
     } else {
         // =============================================================== compute warps
-        for (long long j = 0;; ++j) {
-            const int s = (int)(j % S);
-            const int r = (int)(j % R);
-            mbar_wait_parity(&full_bar[s], (uint32_t)((j / S) & 1));
-            if (j >= R) mbar_wait_parity(&pempty_bar[r], (uint32_t)(((j / R) - 1) & 1));
+        long long pseq = 0;  // part slots used
+        for (long long c = 0;; ++c) {
+            const int cs = (int)(c % C);
+            mbar_wait_parity(&cfull_bar[cs], (uint32_t)((c / C) & 1));
+            const Cmd cmd = cmds[cs];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&cempty_bar[cs]);
+            const int s = cmd.stage;
+            if (cmd.op == kOpP2) {  // hold mode, pass 2 on the held block; no part slot
+                const Item it = meta[s].it;
+                const int valid = meta[s].valid;
+                BlockVals v;
+                load_stage<In>(stages + (size_t)s * kBlockElems, v);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+                op_pass2<V>(v, meta[s].stats, ((meta[s].mask >> warp) & 1u) != 0,
+                            a.y + it.row * a.cols + it.blk * kBlockElems, valid, true);
+                continue;
+            }
+            const int r = (int)(pseq % R);
+            if (pseq >= R) mbar_wait_parity(&pempty_bar[r], (uint32_t)(((pseq / R) - 1) & 1));
+            ++pseq;
             PartSlot& ps = pslot[r];
-            const long long item = meta[s].item;
-            if (item >= total) {  // pass the sentinel on to the retire warp
-                if (warp == 0 && lane == 0) ps.item = item;
+            if (cmd.op == kOpExit) {  // pass the end on to the retire warp
+                if (warp == 0 && lane == 0) ps.item = total;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&pfull_bar[r]);
                 break;
             }
+            mbar_wait_parity(&full_bar[s], cmd.parity);
             const Item it = meta[s].it;
             const int valid = meta[s].valid;
             const float4 st = meta[s].stats;
@@ -253,15 +321,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             float* yb = a.y ? a.y + it.row * a.cols + it.blk * kBlockElems : nullptr;
             BlockVals v;
             if (!(A == kReload && it.phase == 2)) load_stage<In>(stages + (size_t)s * kBlockElems, v);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[s]);  // the stage is free: values are in registers
+            if (cmd.op == kOpItem) {  // stream mode: the values are in registers, free the stage
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+            }
 
             if constexpr (A == kFused) {
                 op_pass1<V>(v, valid, ps.part);
                 asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");  // compute warps only
                 op_fused_tail<V>(v, ps.part, yb, valid, true);
             } else if constexpr (A == kTwoPass || A == kPartial) {
-                if (it.phase == 0) op_pass1<V>(v, valid, ps.part);
+                if (it.phase == 0) op_pass1<V>(v, valid, ps.part);  // kOpP1 (hold) or stream pass 1
                 else op_pass2<V>(v, st, my_clamp, yb, valid, true);
             } else if constexpr (A == kFinish) {
                 op_pass2<V>(v, st, true, yb, valid, true);
@@ -272,7 +342,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 else op_out_reload(st, yb, valid, true);
             }
             if (warp == 0 && lane == 0) {
-                ps.item = item;
+                ps.item = meta[s].item;
                 ps.it = it;
                 ps.mu = st.x;
             }
@@ -287,7 +357,8 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     auto kern = stream_kernel<In, A>;
-    const size_t dyn = (size_t)Ring<In>::S * kBlockElems * sizeof(In);
+    constexpr int S = Ring<In>::S;
+    const size_t dyn = (size_t)S * kBlockElems * sizeof(In);
     static int configured[64];
     if (!configured[dev]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -296,11 +367,14 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     const int64_t resident = device_sms(dev);  // one CTA per SM
     int64_t grid = o.grid_ctas > 0 ? o.grid_ctas : resident;
     if (grid > resident) grid = resident;
+    // hold mode: Two-Pass rows of several blocks that fit the grid's stages four times over
+    a.hold = (A == kTwoPass && !o.no_hold && a.nb >= 2 && a.nb * 4 <= grid * S) ? 1 : 0;
+    if (a.hold) a.total_items = a.rows * a.nb;
     if (grid > a.total_items) grid = a.total_items;
     if (grid < 1) grid = 1;
-    // items a CTA holds between hand-out and retirement: its stages, the prefetched queue chunks
-    // and the part-slot backlog (measured: C4 gains up to L ~ 50 rows, tools/sweep.py)
-    a.L = lookahead_rows(a, grid, Ring<In>::S + 12, o);
+    // stream mode: items a CTA holds between hand-out and retirement (its stages, the prefetched
+    // queue chunks and the part-slot backlog; measured: C4 gains up to L ~ 50 rows)
+    a.L = lookahead_rows(a, grid, S + 12, o);
     kern<<<(unsigned)grid, kStreamThreads, dyn, s>>>(a);
     return cudaGetLastError();
 }

@@ -216,6 +216,21 @@ def test_tma_and_global_load_paths_agree_bitwise(rows, cols, dtype):
         assert np.array_equal(a, b), algo
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", [(64, 32768), (9, 16384 * 5 + 12), (40, 800000)])
+def test_hold_and_reread_schedules_agree_bitwise(rows, cols, dtype):
+    # hold: blocks stay in shared memory between the passes; re-read: pass 2 reloads them
+    x = workloads.ragged_case(rows, cols, -500, 500, seed=6, stream=cols)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    a = to_host(tp.softmax(xd))
+    b = to_host(tp.softmax_ex(xd, disable_hold=True))
+    assert np.array_equal(a, b)
+    if rows * cols <= 2_000_000:
+        assert_parity(x, a, "hold")
+
+
 def test_out_of_domain_blocks_take_the_clamped_path():
     # a row with one huge element, a row entirely below -2^21, a row with +-inf/NaN-free extremes:
     # outputs finite, non-negative, summing to 1; in-domain rows unaffected (reading G11)
