@@ -207,6 +207,26 @@ __device__ __forceinline__ bool wait_flag(const unsigned* f, unsigned want, unsi
     return true;
 }
 
+// Watchdog-guarded mbarrier wait: false when the launch is being aborted (another role gave up,
+// or this wait exceeded kWaitTimeoutNs; `bit` then records which wait).  A bug must never leave
+// the GPU spinning: every role leaves its loop on an abort and the host sees the flags.
+__device__ __forceinline__ bool wait_or_abort(uint64_t* bar, uint32_t parity, unsigned* err, unsigned bit) {
+    if (mbar_try_parity(bar, parity)) return true;
+    const unsigned long long t0 = globaltimer_ns();
+    for (unsigned i = 1;; ++i) {
+        if (mbar_try_parity(bar, parity)) return true;
+        if ((i & 63u) == 0) {
+            if (*reinterpret_cast<volatile unsigned*>(err)) return false;
+            if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                atomicOr(err, bit);
+                return false;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ bool aborted(unsigned* err) { return *reinterpret_cast<volatile unsigned*>(err) != 0; }
+
 __device__ __forceinline__ void exit_and_reset(WsHeader* hdr) {
     __threadfence();
     const unsigned t = atomicAdd(&hdr->exit_ticket, 1u);

@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
 
         auto push = [&](int op, int s, unsigned parity) {
             const int c = (int)(pushed % C);
-            if (pushed >= C) mbar_wait_parity(&cempty_bar[c], (uint32_t)(((pushed / C) - 1) & 1));
+            if (pushed >= C && !wait_or_abort(&cempty_bar[c], (uint32_t)(((pushed / C) - 1) & 1), &hdr->error, 64u))
+                return;
             cmds[c] = Cmd{op, s, parity};
             mbar_arrive(&cfull_bar[c]);
             ++pushed;
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         };
 
         for (;;) {
+            if (aborted(&hdr->error)) return;  // watchdog: every role leaves
             poll();
             bool busy = false;
             for (int s = 0; s < S; ++s) {
@@ -256,11 +258,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         for (long long seq = 0;;) {
             int n = 0;
             if (lane == 0) {
-                mbar_wait_parity(&pfull_bar[seq % R], (uint32_t)((seq / R) & 1));
-                n = 1;
-                while (n < R && mbar_test_parity(&pfull_bar[(seq + n) % R], (uint32_t)(((seq + n) / R) & 1))) ++n;
+                if (wait_or_abort(&pfull_bar[seq % R], (uint32_t)((seq / R) & 1), &hdr->error, 32u)) {
+                    n = 1;
+                    while (n < R && mbar_test_parity(&pfull_bar[(seq + n) % R], (uint32_t)(((seq + n) / R) & 1))) ++n;
+                }
             }
             n = __shfl_sync(0xffffffffu, n, 0);
+            if (n == 0) break;  // aborted
             const bool have = lane < n;
             const PartSlot* ps = &pslot[(seq + lane) % R];
             const long long item = have ? ps->item : total;
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         long long pseq = 0;  // part slots used
         for (long long c = 0;; ++c) {
             const int cs = (int)(c % C);
-            mbar_wait_parity(&cfull_bar[cs], (uint32_t)((c / C) & 1));
+            if (!wait_or_abort(&cfull_bar[cs], (uint32_t)((c / C) & 1), &hdr->error, 8u)) break;
             const Cmd cmd = cmds[cs];
             __syncwarp();
             if (lane == 0) mbar_arrive(&cempty_bar[cs]);
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 continue;
             }
             const int r = (int)(pseq % R);
-            if (pseq >= R) mbar_wait_parity(&pempty_bar[r], (uint32_t)(((pseq / R) - 1) & 1));
+            if (pseq >= R && !wait_or_abort(&pempty_bar[r], (uint32_t)(((pseq / R) - 1) & 1), &hdr->error, 16u)) break;
             ++pseq;
             PartSlot& ps = pslot[r];
             if (cmd.op == kOpExit) {  // pass the end on to the retire warp
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 if (lane == 0) mbar_arrive(&pfull_bar[r]);
                 break;
             }
-            mbar_wait_parity(&full_bar[s], cmd.parity);
+            if (!wait_or_abort(&full_bar[s], cmd.parity, &hdr->error, 4u)) break;
             const Item it = meta[s].it;
             const int valid = meta[s].valid;
             const float4 st = meta[s].stats;
