@@ -297,14 +297,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             if (lane == 0) mbar_arrive(&cempty_bar[cs]);
             const int s = cmd.stage;
             if (cmd.op == kOpP2) {  // hold mode, pass 2 on the held block; no part slot
-                const Item it = meta[s].it;
+                const Item it = meta[s].it;  // read everything before the stage is released
                 const int valid = meta[s].valid;
+                const float4 st = meta[s].stats;
+                const bool my_clamp = ((meta[s].mask >> warp) & 1u) != 0;
                 BlockVals v;
                 load_stage<In>(stages + (size_t)s * kBlockElems, v);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[s]);
-                op_pass2<V>(v, meta[s].stats, ((meta[s].mask >> warp) & 1u) != 0,
-                            a.y + it.row * a.cols + it.blk * kBlockElems, valid, true);
+                op_pass2<V>(v, st, my_clamp, a.y + it.row * a.cols + it.blk * kBlockElems, valid, true);
                 continue;
             }
             const int r = (int)(pseq % R);
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 break;
             }
             if (!wait_or_abort(&full_bar[s], cmd.parity, &hdr->error, 4u)) break;
+            const long long item = meta[s].item;  // read everything before the stage is released
             const Item it = meta[s].it;
             const int valid = meta[s].valid;
             const float4 st = meta[s].stats;
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 else op_out_reload(st, yb, valid, true);
             }
             if (warp == 0 && lane == 0) {
-                ps.item = meta[s].item;
+                ps.item = item;
                 ps.it = it;
                 ps.mu = st.x;
             }
