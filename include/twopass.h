@@ -99,15 +99,20 @@ int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t c
  *   larger values are clamped to it); lookahead_rows = rows of pass 1 kept ahead of
  *   pass 2 (0 = automatic); force_persistent = two-phase schedule even for rows that
  *   fit one block; disable_tma = load blocks with 128-bit global loads instead of TMA
- *   bulk copies into shared memory; disable_hold = re-read every block in pass 2 instead
- *   of keeping rows of a few blocks staged in shared memory between the passes.
+ *   bulk copies into shared memory; schedule = TP_SCHED_AUTO (0), TP_SCHED_STREAM (1:
+ *   every pass-2 block is re-read from L2/HBM) or TP_SCHED_HOLD (2: Two-Pass rows of a
+ *   few blocks stay staged in shared memory between the passes; rows that cannot be held
+ *   fall back to the stream schedule).
  *   Results do not depend on any of these. */
+#define TP_SCHED_AUTO 0
+#define TP_SCHED_STREAM 1
+#define TP_SCHED_HOLD 2
 typedef struct {
     int64_t grid_ctas;
     int64_t lookahead_rows;
     int force_persistent;
     int disable_tma;
-    int disable_hold;
+    int schedule;
 } softmax_opts;
 
 size_t softmax_workspace_bytes(int64_t rows, int64_t cols);

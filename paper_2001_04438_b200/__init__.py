@@ -24,6 +24,7 @@ _SO = os.path.join(_PKG, "libtwopass.so")
 
 TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV = 0, 1, 2, 3
 ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3
+SCHED_AUTO, SCHED_STREAM, SCHED_HOLD = 0, 1, 2  # twopass.h TP_SCHED_*
 IN_F32, IN_BF16 = 0, 1
 
 EXPORTS = [
@@ -42,7 +43,7 @@ class TwoPassError(RuntimeError):
 class SoftmaxOpts(ctypes.Structure):
     _fields_ = [("grid_ctas", ctypes.c_int64), ("lookahead_rows", ctypes.c_int64),
                 ("force_persistent", ctypes.c_int), ("disable_tma", ctypes.c_int),
-                ("disable_hold", ctypes.c_int)]
+                ("schedule", ctypes.c_int)]
 
 
 _lib = None
@@ -114,17 +115,17 @@ def _prep(x: torch.Tensor) -> torch.Tensor:
 
 
 def _opts(grid_ctas: int = 0, lookahead_rows: int = 0, force_persistent: bool = False, disable_tma: bool = False,
-          disable_hold: bool = False):
-    if not (grid_ctas or lookahead_rows or force_persistent or disable_tma or disable_hold):
+          schedule: int = 0):
+    if not (grid_ctas or lookahead_rows or force_persistent or disable_tma or schedule):
         return None
     return ctypes.pointer(SoftmaxOpts(grid_ctas, lookahead_rows, int(force_persistent), int(disable_tma),
-                                      int(disable_hold)))
+                                      int(schedule)))
 
 
 def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | None = None,
                workspace: torch.Tensor | None = None, grid_ctas: int = 0, lookahead_rows: int = 0,
                force_persistent: bool = False, disable_tma: bool = False,
-               disable_hold: bool = False) -> torch.Tensor:
+               schedule: int = 0) -> torch.Tensor:
     """Row-wise softmax over the last dim; fp32 output.  See include/twopass.h."""
     x = _prep(x)
     rows, cols = _rows_cols(x)
@@ -133,7 +134,7 @@ def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | N
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel() *
                                                              workspace.element_size())
     st = lib().softmax_ex(algo, _in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, ws_ptr, ws_bytes,
-                          _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma, disable_hold),
+                          _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma, schedule),
                           _stream())
     _check(st, "softmax")
     return y

@@ -130,7 +130,7 @@ tp::LaunchOpts to_opts(const softmax_opts* o) {
         L.lookahead_rows = o->lookahead_rows;
         L.force_persistent = o->force_persistent;
         L.no_tma = o->disable_tma;
-        L.no_hold = o->disable_hold;
+        L.schedule = o->schedule;
     }
     return L;
 }

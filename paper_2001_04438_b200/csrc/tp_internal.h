@@ -27,7 +27,7 @@ struct LaunchOpts {
     int64_t lookahead_rows = 0;  // 0 = automatic
     int force_persistent = 0;    // two-phase schedule even for single-block rows
     int no_tma = 0;              // global loads instead of TMA staging (testing)
-    int no_hold = 0;             // re-read schedule even for rows that could stay staged
+    int schedule = 0;            // 0 automatic, 1 stream (re-read), 2 hold (twopass.h TP_SCHED_*)
 };
 
 size_t workspace_bytes(int64_t rows, int64_t cols);

@@ -26,8 +26,11 @@
 // pfull[r] (count 16) / pempty[r] (count 1) for the part ring.
 // Deadlock freedom: items are handed out in increasing order; a command is pushed only when
 // its inputs exist (no compute warp ever waits for a row); no role blocks on a row flag; so the
-// smallest unfinished item always progresses.  In hold mode a row must fit in the CTAs' stages
-// many times over (hold_max = grid * S / 4 blocks), so the oldest held row is always complete.
+// smallest unfinished item always progresses.  In hold mode a CTA reserves an item only for a
+// stage that is free or certain to free (its P2 pushed), one item per stage, so every reserved
+// block gets staged; a row must fit in the CTAs' stages (hold_max = grid * S / 4 blocks), so the
+// held blocks cannot all belong to the oldest unreleased row: some stage frees, the queue
+// advances, and that row's remaining blocks get staged.
 #include "tp_ops.cuh"
 
 namespace tp {
@@ -116,14 +119,27 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         const In* x = static_cast<const In*>(a.x);
         const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
         constexpr unsigned long long kChunk = 2;
-        unsigned long long next = atomicAdd(&hdr->counter, kChunk), end = next + kChunk;
-        unsigned long long ahead = atomicAdd(&hdr->counter, kChunk);  // result used one chunk later
+        // stream mode: chunks of kChunk items, the next chunk's atomic in flight
+        unsigned long long next = 0, end = 0, ahead = 0;
+        if (!hold) {
+            next = atomicAdd(&hdr->counter, kChunk);
+            end = next + kChunk;
+            ahead = atomicAdd(&hdr->counter, kChunk);  // result used one chunk later
+        }
         bool exhausted = false;
         long long pushed = 0;
         unsigned use[S];       // issues of each stage so far
-        int state[S];          // 0 free, 1 busy (until its empty barrier completes), 2 waiting for stats
+        int state[S];          // 0 free, 1 busy (until its empty barrier completes), 2 waiting for stats,
+                               // 3 retired (hold mode: its reservation was past the end)
         long long order[S];    // issue sequence of the stage's item (stats are provided in this order)
+        // hold mode: each stage owns one reservation, taken when the stage is certain to free
+        // without waiting on anything (at start, and when its P2 command is pushed).  A CTA
+        // never reserves a block it cannot stage, so the oldest unreleased row always gets all
+        // its blocks staged (a row must not wait on a block queued behind held stages).
+        unsigned long long resv[S];
         for (int s = 0; s < S; ++s) use[s] = 0, state[s] = 0, order[s] = 0;
+        if (hold)
+            for (int s = 0; s < S; ++s) resv[s] = atomicAdd(&hdr->counter, 1ull);
         long long issue_seq = 0;
         int64_t cached_row = -1;
         int cached_phase = -1;
@@ -183,6 +199,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                                       : 0u;
                 state[best] = 1;
                 push(hold ? kOpP2 : kOpItem, best, (use[best] - 1) & 1u);
+                if (hold) resv[best] = atomicAdd(&hdr->counter, 1ull);  // consumed when the stage frees
             }
         };
 
@@ -241,6 +258,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             bool busy = false;
             for (int s = 0; s < S; ++s) {
                 if (state[s] == 1 && mbar_test_parity(&empty_bar[s], (use[s] - 1) & 1u)) state[s] = 0;
+                if (hold) {
+                    if (state[s] == 0) {
+                        if (resv[s] >= (unsigned long long)total) state[s] = 3;
+                        else issue(s, (long long)resv[s]);
+                    }
+                    busy |= state[s] != 3;
+                    continue;
+                }
                 if (state[s] == 0 && !exhausted) {
                     const long long item = take();
                     if (item >= total) exhausted = true;
@@ -248,10 +273,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 }
                 busy |= state[s] != 0;
             }
-            if (exhausted && !busy) break;
+            if ((hold || exhausted) && !busy) break;
         }
         push(kOpExit, 0, 0);
-        if (ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
+        if (!hold && ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
         exit_and_reset(hdr);
     } else if (warp == kRetireWarp) {
         // =============================================================== retire warp
@@ -374,7 +399,7 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     int64_t grid = o.grid_ctas > 0 ? o.grid_ctas : resident;
     if (grid > resident) grid = resident;
     // hold mode: Two-Pass rows of several blocks that fit the grid's stages four times over
-    a.hold = (A == kTwoPass && !o.no_hold && a.nb >= 2 && a.nb * 4 <= grid * S) ? 1 : 0;
+    a.hold = (A == kTwoPass && o.schedule == 2 && a.nb >= 2 && a.nb * 4 <= grid * S) ? 1 : 0;
     if (a.hold) a.total_items = a.rows * a.nb;
     if (grid > a.total_items) grid = a.total_items;
     if (grid < 1) grid = 1;

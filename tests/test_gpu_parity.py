@@ -224,8 +224,8 @@ def test_hold_and_reread_schedules_agree_bitwise(rows, cols, dtype):
     if dtype == "bf16":
         x = workloads.to_bf16(x)
     xd = to_dev(x)
-    a = to_host(tp.softmax(xd))
-    b = to_host(tp.softmax_ex(xd, disable_hold=True))
+    a = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_HOLD))
+    b = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
     assert np.array_equal(a, b)
     if rows * cols <= 2_000_000:
         assert_parity(x, a, "hold")

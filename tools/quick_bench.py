@@ -55,7 +55,7 @@ def main():
             t = float(np.median(ts))
             gbs = BYTES[(algo, cfg.dtype)] * cfg.elements / t / 1e9
             rec = dict(config=key, algo=algo, median_us=t * 1e6, min_us=min(ts) * 1e6, alg_GBps=gbs,
-                       elems_per_s=cfg.elements / t)
+                       elems_per_s=cfg.elements / t, watchdog=tp.watchdog_flags())
             out.append(rec)
             print(json.dumps(rec), flush=True)
         del xd, y

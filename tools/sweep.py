@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--lookaheads", default="0")
     ap.add_argument("--grids", default="0")
     ap.add_argument("--reps", type=int, default=15)
-    ap.add_argument("--no-hold", action="store_true")
+    ap.add_argument("--schedule", type=int, default=0)
     args = ap.parse_args()
     cfg = workloads.CONFIGS[args.config]
     x = workloads.generate(args.config)
@@ -37,7 +37,7 @@ def main():
     for g in [int(v) for v in args.grids.split(",")]:
         for la in [int(v) for v in args.lookaheads.split(",")]:
             run = lambda: tp.softmax_ex(xd, ALGO[args.algo], out=y, grid_ctas=g, lookahead_rows=la,
-                                                disable_hold=args.no_hold)  # noqa: E731
+                                                schedule=args.schedule)  # noqa: E731
             for _ in range(3):
                 run()
             ts = []
@@ -51,7 +51,7 @@ def main():
                 ts.append(s.elapsed_time(e) * 1e3)
             t = float(np.median(ts))
             print(json.dumps({"config": args.config, "algo": args.algo, "grid": g, "lookahead": la,
-                              "hints": os.environ.get("TP_L2_HINTS", "1"), "hold": not args.no_hold, "median_us": round(t, 2),
+                              "hints": os.environ.get("TP_L2_HINTS", "1"), "schedule": args.schedule, "median_us": round(t, 2),
                               "alg_GBps": round(BYTES[cfg.dtype] * cfg.elements / t / 1e3, 1)}), flush=True)
 
 
