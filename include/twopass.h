@@ -100,19 +100,25 @@ int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t c
  *   pass 2 (0 = automatic); force_persistent = two-phase schedule even for rows that
  *   fit one block; disable_tma = load blocks with 128-bit global loads instead of TMA
  *   bulk copies into shared memory; schedule = TP_SCHED_AUTO (0), TP_SCHED_STREAM (1:
- *   every pass-2 block is re-read from L2/HBM) or TP_SCHED_HOLD (2: Two-Pass rows of a
- *   few blocks stay staged in shared memory between the passes; rows that cannot be held
- *   fall back to the stream schedule).
- *   Results do not depend on any of these. */
+ *   a persistent grid shares every row, pass-2 blocks are re-read from L2/HBM),
+ *   TP_SCHED_HOLD (2: as STREAM, but Two-Pass rows of a few blocks stay staged in shared
+ *   memory between the passes) or TP_SCHED_CLUSTER (3: Two-Pass rows of 2..256 blocks,
+ *   one thread-block cluster per row, the row's block values exchanged through distributed
+ *   shared memory, pass 2 from shared memory / L2; AUTO picks it when the cluster's L2
+ *   working set fits); a schedule that does not apply falls back to STREAM;
+ *   cluster_size = CTAs per row for TP_SCHED_CLUSTER (0 = automatic; 1, 2, 4 or 8).
+ *   Results do not depend on any of these (bit-identical outputs). */
 #define TP_SCHED_AUTO 0
 #define TP_SCHED_STREAM 1
 #define TP_SCHED_HOLD 2
+#define TP_SCHED_CLUSTER 3
 typedef struct {
     int64_t grid_ctas;
     int64_t lookahead_rows;
     int force_persistent;
     int disable_tma;
     int schedule;
+    int cluster_size;
 } softmax_opts;
 
 size_t softmax_workspace_bytes(int64_t rows, int64_t cols);
@@ -133,6 +139,22 @@ int softmax_f32_host(const float* hx, float* hy, int64_t rows, int64_t cols);
 int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t cols);
 
 /* ---- status ---------------------------------------------------------------- */
+/* What the last launch issued by this host thread ran (diagnostics; no device work):
+ * kernel = 1 general (any alignment), 2 stream (persistent grid), 3 cluster (one
+ * thread-block cluster per row); variant = the kernel's operation (0 Two-Pass, 1 partial,
+ * 2 Recompute, 3 Reload, 4 single-block rows, 5 finish); grid_ctas; cluster_size (kernel 3);
+ * lookahead_rows (kernel 1/2); hold = blocks kept staged between the passes (2: per row,
+ * 3: per CTA and row).  Returns TP_EINVAL for a NULL pointer. */
+typedef struct {
+    int kernel;
+    int variant;
+    int64_t grid_ctas;
+    int cluster_size;
+    int64_t lookahead_rows;
+    int hold;
+} softmax_plan;
+int softmax_last_plan(softmax_plan* out);
+
 const char* softmax_status_str(int status);
 int softmax_last_cuda_error(void); /* cudaError_t of the last TP_ECUDA on this thread */
 /* Watchdog flags of a workspace (NULL = this device's internal one); synchronous.
@@ -149,6 +171,18 @@ int softmax_watchdog_flags(const void* workspace, int reset);
  *        4: the kernels' 2^k for integer k (MUFU.EX2, .ftz) -> out0              */
 int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                 cudaStream_t stream);
+
+/* Compute-only throughput probe (roofline evidence, not part of the method): `ctas` CTAs of
+ * 512 threads each run `reps` times over one shared-memory block of 16384 synthetic logits:
+ * what = 0 pass 1, 1 pass 2 (no store), 2 both; 3-6 instruction throughput (64 per thread
+ * per rep: 3 FFMA2, 4 FFMA2 with an immediate, 5 FFMA, 6 integer add-max + shift).  sink: device, ctas*16 floats (results are
+ * meaningless; they keep the work alive).  in_dtype TP_IN_F32 / TP_IN_BF16. */
+/* Development: a device buffer of 16 uint64 counters (zeroed by the caller) that later
+ * cluster-kernel launches accumulate per-role clock cycles into, summed over CTAs
+ * (tools/prof_roles.py documents the slots); NULL switches it off. */
+int tp_set_profile_buffer(void* device_counters);
+
+int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ _SO = os.path.join(_PKG, "libtwopass.so")
 
 TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV = 0, 1, 2, 3
 ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3
-SCHED_AUTO, SCHED_STREAM, SCHED_HOLD = 0, 1, 2  # twopass.h TP_SCHED_*
+SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER = 0, 1, 2, 3  # twopass.h TP_SCHED_*
 IN_F32, IN_BF16 = 0, 1
 
 EXPORTS = [
@@ -32,7 +32,8 @@ EXPORTS = [
     "softmax3_recompute_bf16_f32", "softmax3_reload_bf16_f32", "softmax_f32_partial",
     "softmax_bf16_partial", "softmax_f32_finish", "softmax_bf16_f32_finish", "softmax_workspace_bytes",
     "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_f32_host", "softmax_bf16_f32_host",
-    "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "tp_debug_op",
+    "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
+    "tp_bench_compute", "tp_set_profile_buffer",
 ]
 
 
@@ -43,8 +44,15 @@ class TwoPassError(RuntimeError):
 class SoftmaxOpts(ctypes.Structure):
     _fields_ = [("grid_ctas", ctypes.c_int64), ("lookahead_rows", ctypes.c_int64),
                 ("force_persistent", ctypes.c_int), ("disable_tma", ctypes.c_int),
-                ("schedule", ctypes.c_int)]
+                ("schedule", ctypes.c_int), ("cluster_size", ctypes.c_int)]
 
+
+class SoftmaxPlan(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int), ("variant", ctypes.c_int), ("grid_ctas", ctypes.c_int64),
+                ("cluster_size", ctypes.c_int), ("lookahead_rows", ctypes.c_int64), ("hold", ctypes.c_int)]
+
+
+KERNEL_NAMES = {0: "none", 1: "general", 2: "stream", 3: "cluster"}
 
 _lib = None
 
@@ -76,6 +84,9 @@ def lib() -> ctypes.CDLL:
         L.softmax_status_str.restype = ctypes.c_char_p
         L.tp_debug_op.argtypes = [ci, vp, vp, vp, vp, i64, vp]
         L.softmax_watchdog_flags.argtypes = [vp, ci]
+        L.tp_set_profile_buffer.argtypes = [vp]
+        L.tp_bench_compute.argtypes = [ci, ci, i64, ci, vp, vp]
+        L.softmax_last_plan.argtypes = [ctypes.POINTER(SoftmaxPlan)]
         _lib = L
     return _lib
 
@@ -115,17 +126,17 @@ def _prep(x: torch.Tensor) -> torch.Tensor:
 
 
 def _opts(grid_ctas: int = 0, lookahead_rows: int = 0, force_persistent: bool = False, disable_tma: bool = False,
-          schedule: int = 0):
-    if not (grid_ctas or lookahead_rows or force_persistent or disable_tma or schedule):
+          schedule: int = 0, cluster_size: int = 0):
+    if not (grid_ctas or lookahead_rows or force_persistent or disable_tma or schedule or cluster_size):
         return None
     return ctypes.pointer(SoftmaxOpts(grid_ctas, lookahead_rows, int(force_persistent), int(disable_tma),
-                                      int(schedule)))
+                                      int(schedule), int(cluster_size)))
 
 
 def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | None = None,
                workspace: torch.Tensor | None = None, grid_ctas: int = 0, lookahead_rows: int = 0,
                force_persistent: bool = False, disable_tma: bool = False,
-               schedule: int = 0) -> torch.Tensor:
+               schedule: int = 0, cluster_size: int = 0) -> torch.Tensor:
     """Row-wise softmax over the last dim; fp32 output.  See include/twopass.h."""
     x = _prep(x)
     rows, cols = _rows_cols(x)
@@ -134,7 +145,7 @@ def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | N
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel() *
                                                              workspace.element_size())
     st = lib().softmax_ex(algo, _in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, ws_ptr, ws_bytes,
-                          _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma, schedule),
+                          _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma, schedule, cluster_size),
                           _stream())
     _check(st, "softmax")
     return y
@@ -199,6 +210,14 @@ def softmax_host(hx: torch.Tensor, hy: torch.Tensor | None = None) -> torch.Tens
     f = lib().softmax_f32_host if _in_dtype(hx) == IN_F32 else lib().softmax_bf16_f32_host
     _check(f(hx.data_ptr(), hy.data_ptr(), rows, cols), "softmax_host")
     return hy
+
+
+def last_plan() -> dict:
+    """What the last launch of this host thread ran (kernel, grid, cluster size, ...)."""
+    p = SoftmaxPlan()
+    _check(lib().softmax_last_plan(ctypes.byref(p)), "softmax_last_plan")
+    return {"kernel": KERNEL_NAMES.get(p.kernel, str(p.kernel)), "variant": p.variant, "grid_ctas": p.grid_ctas,
+            "cluster_size": p.cluster_size, "lookahead_rows": p.lookahead_rows, "hold": p.hold}
 
 
 def watchdog_flags(workspace: torch.Tensor | None = None, reset: bool = True) -> int:

@@ -131,6 +131,7 @@ tp::LaunchOpts to_opts(const softmax_opts* o) {
         L.force_persistent = o->force_persistent;
         L.no_tma = o->disable_tma;
         L.schedule = o->schedule;
+        L.cluster_size = o->cluster_size;
     }
     return L;
 }
@@ -384,6 +385,18 @@ const char* softmax_status_str(int status) {
 }
 int softmax_last_cuda_error(void) { return g_last_cuda_error; }
 
+int softmax_last_plan(softmax_plan* out) {
+    if (!out) return TP_EINVAL;
+    const tp::Plan& p = tp::last_plan();
+    out->kernel = p.kernel;
+    out->variant = p.variant;
+    out->grid_ctas = p.grid_ctas;
+    out->cluster_size = p.cluster_size;
+    out->lookahead_rows = p.lookahead_rows;
+    out->hold = p.hold;
+    return TP_OK;
+}
+
 int softmax_watchdog_flags(const void* workspace, int reset) {
     const void* ws = workspace;
     if (!ws) {
@@ -400,6 +413,18 @@ int softmax_watchdog_flags(const void* workspace, int reset) {
         cudaMemcpy((char*)ws + offsetof(tp::WsHeader, error), &z, sizeof(z), cudaMemcpyHostToDevice);
     }
     return (int)h.error;
+}
+
+int tp_set_profile_buffer(void* p) {
+    tp::set_profile_buffer(p);
+    return TP_OK;
+}
+
+int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink, cudaStream_t stream) {
+    if (what < 0 || what > 9 || ctas < 1 || reps < 1 || !sink || (in_dtype != TP_IN_F32 && in_dtype != TP_IN_BF16))
+        return TP_EINVAL;
+    cudaError_t e = tp::launch_bench_compute(what, in_dtype == TP_IN_BF16, ctas, reps, sink, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 
 int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,

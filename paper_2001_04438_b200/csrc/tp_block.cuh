@@ -118,34 +118,102 @@ __device__ __forceinline__ void store_block(float* yb, int valid, bool vec, cons
 // in 4 groups of 8 elements.  Masked elements are (m, n) = (0, -inf).
 template <int V, bool FULL, bool CLAMP>
 __device__ __forceinline__ Pair pass1_thread(const BlockVals& r, int valid) {
-    Acc acc = acc_init();
+    AccV acc = accv_init();
 #pragma unroll
     for (int g = 0; g < kPerThread / 8; ++g) {
-        float2 m[4], n[4];
+        float2 m[4], v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            ext_exp2<CLAMP>(make_float2(r.v[8 * g + 2 * j], r.v[8 * g + 2 * j + 1]), m[j], n[j]);
-            if (!FULL) {
-                const float ninf = -__int_as_float(0x7f800000);
-                if (!(elem_off<V>(8 * g + 2 * j) < valid)) { m[j].x = 0.0f; n[j].x = ninf; }
-                if (!(elem_off<V>(8 * g + 2 * j + 1) < valid)) { m[j].y = 0.0f; n[j].y = ninf; }
+            ext_exp2v<CLAMP>(make_float2(r.v[8 * g + 2 * j], r.v[8 * g + 2 * j + 1]), m[j], v[j]);
+            if (!FULL) {  // masked: m = 0 with v = 0 (scale 0, never the max)
+                if (!(elem_off<V>(8 * g + 2 * j) < valid)) { m[j].x = 0.0f; v[j].x = 0.0f; }
+                if (!(elem_off<V>(8 * g + 2 * j + 1) < valid)) { m[j].y = 0.0f; v[j].y = 0.0f; }
             }
         }
-        acc_add8(acc, m, n);
+        acc_add8v(acc, m, v);
     }
-    return acc_pair(acc);
+    return accv_pair(acc);
+}
+
+// Variant: the thread's largest exponent first (one FFMA2 per pair), then every element scaled
+// to it and summed into 4 independent accumulators (no serial rescaling chain).
+template <int V, bool FULL, bool CLAMP>
+__device__ __forceinline__ Pair pass1_thread_v2(const BlockVals& r, int valid) {
+    float vmax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kPerThread; i += 2) {
+        float2 x = make_float2(r.v[i], r.v[i + 1]);
+        if (CLAMP) {
+            x.x = fminf(fmaxf(x.x, -kXClamp), kXClamp);
+            x.y = fminf(fmaxf(x.y, -kXClamp), kXClamp);
+        }
+        float2 v = ffma2(x, bc2(kLog2e), bc2(kMagic));
+        if (!FULL) {
+            if (!(elem_off<V>(i) < valid)) v.x = 0.0f;
+            if (!(elem_off<V>(i + 1) < valid)) v.y = 0.0f;
+        }
+        vmax = fmaxf(vmax, fmaxf(v.x, v.y));
+    }
+    const int c = __float_as_int(vmax) - 127;
+    float2 s[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+    for (int i = 0; i < kPerThread; i += 2) {
+        float2 m, v;
+        ext_exp2v<CLAMP>(make_float2(r.v[i], r.v[i + 1]), m, v);
+        if (!FULL) {
+            if (!(elem_off<V>(i) < valid)) { m.x = 0.0f; v.x = 0.0f; }
+            if (!(elem_off<V>(i + 1) < valid)) { m.y = 0.0f; v.y = 0.0f; }
+        }
+        const int j = (i / 2) & 3;
+        s[j] = ffma2(m, make_float2(pow2_bits(__float_as_int(v.x) - c), pow2_bits(__float_as_int(v.y) - c)), s[j]);
+    }
+    const float2 t = fadd2(fadd2(s[0], s[1]), fadd2(s[2], s[3]));
+    const float n = vmax != 0.0f ? __fsub_rn(vmax, kMagic) : -kFltMax;
+    return Pair{__fadd_rn(t.x, t.y), n};
+}
+
+// Pass 2 variant with lambda' folded into the polynomial (coefficients lambda' c_i, per call).
+template <bool CLAMP>
+__device__ __forceinline__ void pass2_thread_v2(BlockVals& r, float nsum1, float lam_half) {
+    const int c = magic_bits() + __float2int_rn(nsum1) - 127;
+    const float l1 = __fmul_rn(lam_half, kC1), l2 = __fmul_rn(lam_half, kC2), l3 = __fmul_rn(lam_half, kC3),
+                l4 = __fmul_rn(lam_half, kC4), l5 = __fmul_rn(lam_half, kC5);
+#pragma unroll
+    for (int i = 0; i < kPerThread; i += 2) {
+        float2 x = make_float2(r.v[i], r.v[i + 1]);
+        if (CLAMP) {
+            x.x = fminf(fmaxf(x.x, -kXClamp), kXClamp);
+            x.y = fminf(fmaxf(x.y, -kXClamp), kXClamp);
+        }
+        const float2 v = ffma2(x, bc2(kLog2e), bc2(kMagic));
+        const float2 n = fadd2(v, bc2(-kMagic));
+        float2 t = ffma2(n, bc2(-kLn2Hi), x);
+        t = ffma2(n, bc2(-kLn2Lo), t);
+        float2 p = ffma2(bc2(l5), t, bc2(l4));
+        p = ffma2(p, t, bc2(l3));
+        p = ffma2(p, t, bc2(l2));
+        p = ffma2(p, t, bc2(l1));
+        p = ffma2(p, t, bc2(lam_half));
+        const float2 s = make_float2(pow2_bits(__float_as_int(v.x) - c), pow2_bits(__float_as_int(v.y) - c));
+        const float2 y = fmul2(p, s);
+        r.v[i] = y.x;
+        r.v[i + 1] = y.y;
+    }
 }
 
 // Pass 2 in place: y = (m * lambda') * 2^(n - (n_sum - 1)), lambda' = 0.5 / m_sum
 // (PAPER.md:166-168 with reading G9: never form lambda * 2^k first).
 template <bool CLAMP>
 __device__ __forceinline__ void pass2_thread(BlockVals& r, float nsum1, float lam_half) {
+    // 2^(n - nsum1) = pow2_bits(bits(v) - c), flushed to 0 below 2^-126 (reading G9);
+    // |nsum1| <= 3025526 (reading G11), exactly an int
+    const int c = magic_bits() + __float2int_rn(nsum1) - 127;
 #pragma unroll
     for (int i = 0; i < kPerThread; i += 2) {
-        float2 m, n;
-        ext_exp2<CLAMP>(make_float2(r.v[i], r.v[i + 1]), m, n);
-        const float2 k = fadd2(n, bc2(-nsum1));
-        const float2 y = fmul2(fmul2(m, bc2(lam_half)), make_float2(ex2_ftz(k.x), ex2_ftz(k.y)));
+        float2 m, v;
+        ext_exp2v<CLAMP>(make_float2(r.v[i], r.v[i + 1]), m, v);
+        const float2 s = make_float2(pow2_bits(__float_as_int(v.x) - c), pow2_bits(__float_as_int(v.y) - c));
+        const float2 y = fmul2(fmul2(m, bc2(lam_half)), s);
         r.v[i] = y.x;
         r.v[i + 1] = y.y;
     }
@@ -220,6 +288,16 @@ __device__ __forceinline__ bool warp_pass1(const BlockVals& r, int valid, Pair* 
     if (clamped) acc = pass1_thread<V, false, true>(r, valid);
     *wp = warp_tree_pairs(acc);
     return clamped;
+}
+
+// The same without the warp tree: this thread's pair (after the warp's clamp decision, which
+// *clamped receives); the tree is left to the caller (tp_rowcl.cu's tree warp).
+template <int V>
+__device__ __forceinline__ Pair thread_pass1(const BlockVals& r, int valid, bool* clamped) {
+    Pair acc = valid == kBlockElems ? pass1_thread<V, true, false>(r, valid) : pass1_thread<V, false, false>(r, valid);
+    *clamped = __any_sync(0xffffffffu, acc_out_of_domain(acc));
+    if (*clamped) acc = pass1_thread<V, false, true>(r, valid);
+    return acc;
 }
 
 // ---- Three-Pass helpers (Alg. 1/2)

@@ -108,6 +108,31 @@ __device__ __forceinline__ void ext_exp2(float2 x, float2& m, float2& n) {
     m = ffma2(p, t, bc2(1.0f));
 }
 
+// The same, also returning v = x log2e + 1.5*2^23 (the rounding sum): for |n| < 2^22 its bits
+// are bits(1.5*2^23) + n, so 2^(n - c) can be built with integer operations (pow2_bits).
+template <bool CLAMP>
+__device__ __forceinline__ void ext_exp2v(float2 x, float2& m, float2& v) {
+    if (CLAMP) {
+        x.x = fminf(fmaxf(x.x, -kXClamp), kXClamp);
+        x.y = fminf(fmaxf(x.y, -kXClamp), kXClamp);
+    }
+    v = ffma2(x, bc2(kLog2e), bc2(kMagic));
+    const float2 n = fadd2(v, bc2(-kMagic));
+    float2 t = ffma2(n, bc2(-kLn2Hi), x);
+    t = ffma2(n, bc2(-kLn2Lo), t);
+    float2 p = ffma2(bc2(kC5), t, bc2(kC4));
+    p = ffma2(p, t, bc2(kC3));
+    p = ffma2(p, t, bc2(kC2));
+    p = ffma2(p, t, bc2(kC1));
+    m = ffma2(p, t, bc2(1.0f));
+}
+
+// 2^(d - 127) for an integer d <= 255, flushed to +0 for d <= 0: the value ex2_ftz gives for the
+// integer exponent d - 127 (reading G5), built in the exponent field on the integer pipe
+// (no MUFU): max, shift.  With d = bits(v) - c this is 2^(n - (c - bits(1.5*2^23) + 127)).
+__device__ __forceinline__ float pow2_bits(int d) { return __int_as_float(max(d, 0) << 23); }
+__device__ __forceinline__ int magic_bits() { return __float_as_int(kMagic); }
+
 // Exp with reconstruction for the Three-Pass comparators (Alg. 4), argument
 // d = x - mu <= 0 (PAPER.md:258 footnote): y = p * s, s = 2^n or 0 below 2^-126 (reading G5).
 __device__ __forceinline__ float2 exp_flush2(float2 d) {
@@ -164,6 +189,34 @@ __device__ __forceinline__ void acc_add8(Acc& acc, const float2 (&m)[4], const f
 }
 
 __device__ __forceinline__ Pair acc_pair(const Acc& a) { return Pair{__fadd_rn(a.m.x, a.m.y), a.n}; }
+
+// The same accumulator keyed by vb = bits of the rounding sum v of its exponent (ext_exp2v;
+// 0 = no element yet).  acc_add8v computes exactly what acc_add8 computes (the scales are the
+// same powers of two, flushed below 2^-126 alike) with the scales built on the integer pipe.
+struct AccV {
+    float2 m;
+    int vb;
+};
+__device__ __forceinline__ AccV accv_init() { return AccV{make_float2(0.0f, 0.0f), 0}; }
+
+__device__ __forceinline__ void acc_add8v(AccV& acc, const float2 (&m)[4], const float2 (&v)[4]) {
+    float vmax = __int_as_float(acc.vb);  // v >= 2^22 > 0 for every element: float order = bits order
+#pragma unroll
+    for (int j = 0; j < 4; ++j) vmax = fmaxf(vmax, fmaxf(v[j].x, v[j].y));
+    const int c = __float_as_int(vmax) - 127;  // pow2_bits(bits(v_i) - c) = 2^(n_i - n_max)
+    float2 s = fmul2(acc.m, bc2(pow2_bits(acc.vb - c)));
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        s = ffma2(m[j], make_float2(pow2_bits(__float_as_int(v[j].x) - c), pow2_bits(__float_as_int(v[j].y) - c)), s);
+    acc.m = s;
+    acc.vb = __float_as_int(vmax);
+}
+
+// (m, n) of the accumulator; no element -> (0, -FLT_MAX) as acc_init.
+__device__ __forceinline__ Pair accv_pair(const AccV& a) {
+    const float n = a.vb ? __fsub_rn(__int_as_float(a.vb), kMagic) : -kFltMax;
+    return Pair{__fadd_rn(a.m.x, a.m.y), n};
+}
 
 // ----------------------------------------------------------------------------- CTA trees
 // Perfect binary tree over the CTA's kThreads values in thread order (left = lower index).
@@ -253,6 +306,20 @@ __device__ __forceinline__ Pair seq_tree_pairs(int c, LeafFn leaf) {
         ++top;
     }
     return st[0];
+}
+
+// The same perfect tree over N (power of two, compile time) leaves, fully unrolled: registers
+// only, log2(N) levels of independent merges.
+template <int N, typename LeafFn>
+__device__ __forceinline__ Pair tree_pairs_n(LeafFn leaf) {
+    Pair t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = leaf(i);
+#pragma unroll
+    for (int o = 1; o < N; o <<= 1)
+#pragma unroll
+        for (int i = 0; i + o < N; i += 2 * o) t[i] = pair_merge(t[i], t[i + o]);
+    return t[0];
 }
 
 template <typename LeafFn>

@@ -1,6 +1,6 @@
 // Unit-test kernels: expose the device building blocks (tp_common.cuh) element by element so
 // tests can check them against the oracle's plain definitions and exact pair arithmetic.
-#include "tp_common.cuh"
+#include "tp_block.cuh"
 #include "tp_internal.h"
 
 namespace tp {
@@ -26,6 +26,89 @@ __global__ void debug_kernel(int what, const float* a, const float* b, float* o0
         case 4: o0[i] = ex2_ftz(a[i]); break;
         default: break;
     }
+}
+
+// Compute-only throughput of the per-block operations (development / roofline evidence): each
+// CTA of 512 threads runs `reps` times over one shared-memory block of synthetic logits:
+// what = 0 pass 1 (ExtExp + pair accumulation + warp tree), 1 pass 2 (ExtExp + output
+// scaling, no store), 2 both.  One value per CTA goes to `sink` so nothing is optimised away.
+template <typename In>
+__global__ void __launch_bounds__(kThreads, 1) bench_compute_kernel(int what, int reps, float* sink) {
+    constexpr int V = InTraits<In>::V;
+    extern __shared__ __align__(16) unsigned char dsm_probe[];
+    In* blk = reinterpret_cast<In*>(dsm_probe);
+    for (int i = threadIdx.x; i < kBlockElems; i += kThreads) {
+        const float v = (float)((i * 7919 + blockIdx.x * 104729) % 20011) * 0.05f - 500.0f;
+        if constexpr (sizeof(In) == 4) blk[i] = v;
+        else blk[i] = (uint16_t)(__float_as_uint(v) >> 16);
+    }
+    __syncthreads();
+    float acc = 0.0f;
+    if (what >= 3 && what <= 6) {  // instruction throughput: 8 independent chains per thread, 64 ops per rep
+        float2 c[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = make_float2(blk[threadIdx.x + j], blk[threadIdx.x + 8 + j]);
+        const float2 mul = make_float2(blk[5], blk[6]), add = make_float2(blk[7], blk[8]);
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (what == 3) c[j] = ffma2(c[j], mul, add);               // FFMA2 3-register
+                    else if (what == 4) c[j] = ffma2(c[j], mul, bc2(0.5f));    // FFMA2 immediate addend
+                    else if (what == 5) c[j].x = __fmaf_rn(c[j].x, mul.x, add.x);  // scalar FFMA
+                    else c[j] = make_float2(__int_as_float(max(__float_as_int(c[j].x) - 3, 0) << 1), c[j].y);  // ALU
+                }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += c[j].x + c[j].y;
+        if ((threadIdx.x & 31) == 0) sink[blockIdx.x * kWarps + (threadIdx.x >> 5)] = acc;
+        return;
+    }
+    for (int r = 0; r < reps; ++r) {
+        BlockVals v;
+        load_stage<In>(blk, v);
+        const float off = acc * 0.0f + (float)(r & 1);  // defeats hoisting the loop-invariant work
+#pragma unroll
+        for (int i = 0; i < kPerThread; i += 2) {
+            const float2 t = fadd2(make_float2(v.v[i], v.v[i + 1]), bc2(off));
+            v.v[i] = t.x;
+            v.v[i + 1] = t.y;
+        }
+        if (what == 7) {
+            acc += pass1_thread_v2<V, true, false>(v, kBlockElems).m;
+        } else if (what == 8) {
+            pass2_thread_v2<false>(v, acc * 1e-30f + 300.0f, 0.25f);
+#pragma unroll
+            for (int i = 0; i < kPerThread; ++i) acc += v.v[i];
+        } else if (what == 9) {
+            acc += pass1_thread<V, true, false>(v, kBlockElems).m;
+        }
+        if (what >= 7) continue;
+        if (what != 1) {
+            Pair wp;
+            warp_pass1<V>(v, kBlockElems, &wp);
+            acc += wp.m;
+        }
+        if (what != 0) {
+            pass2_thread<false>(v, acc * 1e-30f + 300.0f, 0.25f);
+#pragma unroll
+            for (int i = 0; i < kPerThread; ++i) acc += v.v[i];
+        }
+    }
+    if ((threadIdx.x & 31) == 0) sink[blockIdx.x * kWarps + (threadIdx.x >> 5)] = acc;
+}
+
+cudaError_t launch_bench_compute(int what, int in_bf16, int64_t ctas, int reps, float* sink, cudaStream_t s) {
+    const int dyn = kBlockElems * (in_bf16 ? 2 : 4);
+    if (in_bf16) {
+        cudaFuncSetAttribute(bench_compute_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        bench_compute_kernel<uint16_t><<<(unsigned)ctas, kThreads, dyn, s>>>(what, reps, sink);
+    } else {
+        cudaFuncSetAttribute(bench_compute_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        bench_compute_kernel<float><<<(unsigned)ctas, kThreads, dyn, s>>>(what, reps, sink);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_debug(int what, const float* a, const float* b, float* o0, float* o1, int64_t count,

@@ -27,8 +27,23 @@ struct LaunchOpts {
     int64_t lookahead_rows = 0;  // 0 = automatic
     int force_persistent = 0;    // two-phase schedule even for single-block rows
     int no_tma = 0;              // global loads instead of TMA staging (testing)
-    int schedule = 0;            // 0 automatic, 1 stream (re-read), 2 hold (twopass.h TP_SCHED_*)
+    int schedule = 0;            // 0 automatic, 1 stream (re-read), 2 hold, 3 cluster (twopass.h TP_SCHED_*)
+    int cluster_size = 0;        // cluster schedule: CTAs per row (0 = automatic)
 };
+
+// What the last launch on this thread ran (softmax_last_plan in twopass.h).
+struct Plan {
+    int kernel = 0;           // 1 general, 2 stream, 3 cluster
+    int variant = 0;          // tp_sched.cuh Algo of the kernel instance
+    int64_t grid_ctas = 0;
+    int cluster_size = 0;
+    int64_t lookahead_rows = 0;
+    int hold = 0;
+};
+Plan& last_plan();
+// development: cycle counters of the cluster kernel's roles (kProf* in tp_rowcl.cu), or null
+void set_profile_buffer(void* p);
+unsigned long long* profile_buffer();
 
 size_t workspace_bytes(int64_t rows, int64_t cols);
 // The control region's layout depends on (rows, cols): it must be re-zeroed whenever a
@@ -45,5 +60,6 @@ cudaError_t launch_finish(int in_bf16, const void* x, float* y, int64_t rows, in
 // debug / unit-test kernels (tp_debug.cu)
 cudaError_t launch_debug(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                          cudaStream_t s);
+cudaError_t launch_bench_compute(int what, int in_bf16, int64_t ctas, int reps, float* sink, cudaStream_t s);
 
 }  // namespace tp

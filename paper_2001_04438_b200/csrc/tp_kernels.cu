@@ -123,6 +123,13 @@ __global__ void __launch_bounds__(kThreads, 1) general_kernel(const KArgs a) {
 }
 
 // ----------------------------------------------------------------------------- host launchers
+static unsigned long long* g_prof = nullptr;
+void set_profile_buffer(void* p) { g_prof = static_cast<unsigned long long*>(p); }
+unsigned long long* profile_buffer() { return g_prof; }
+
+thread_local Plan g_plan;
+Plan& last_plan() { return g_plan; }
+
 static int g_num_sms[64];
 
 int device_sms(int dev) {
@@ -164,6 +171,7 @@ static cudaError_t launch_general(KArgs a, const LaunchOpts& o, cudaStream_t s) 
     if (grid > a.total_items) grid = a.total_items;
     if (grid < 1) grid = 1;
     a.L = lookahead_rows(a, grid, 2, o);
+    last_plan() = Plan{1, A, grid, 0, a.L, 0};
     kern<<<(unsigned)grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
@@ -187,7 +195,15 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
         return e ? atoi(e) : 1;
     }();
     a.l2_hints = hints;
-    if (a.vec && !o.no_tma) return launch_stream<In, A>(a, o, s);
+    a.prof = profile_buffer();
+    if (a.vec && !o.no_tma) {
+        // Two-Pass rows of a few blocks: one cluster per row, pass 2 from shared memory / L2
+        if (A == kTwoPass && (o.schedule == 0 || o.schedule == 3)) {
+            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size);
+            if (CL) return launch_rowcl<In>(a, CL, o, s);
+        }
+        return launch_stream<In, A>(a, o, s);
+    }
     return launch_general<In, A>(a, o, s);
 }
 

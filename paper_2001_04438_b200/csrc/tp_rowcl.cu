@@ -1,0 +1,581 @@
+// Row-cluster kernel: Two-Pass softmax (Alg. 3) over rows of 2..kClMaxNb
+// blocks, one thread-block cluster per row at a time, for 16-byte aligned rows.
+//
+// Why: the stream kernel (tp_stream.cu) spreads a row's blocks over the whole grid, so a row's
+// statistics exist only after a grid-wide publication (global atomics, fences, flag polling:
+// several microseconds), and pass 2 must trail pass 1 by tens of rows, too far for the row to
+// still be in L2: pass 2 re-reads HBM (12 B per element of DRAM traffic).  Here a cluster of CL
+// CTAs owns a row; each CTA streams its contiguous share of the row's blocks through pass 1,
+// the CTAs exchange their block values through distributed shared memory (one remote store
+// per block and one remote mbarrier arrive per CTA pair), and pass 2 starts a few microseconds
+// after the row's last load: the last H blocks of each CTA are still staged in shared memory
+// (read once), the others come back from L2.  DRAM traffic approaches the compulsory
+// 8 B per fp32 element (one read, one write).
+//
+// Roles per CTA (18 warps, as the stream kernel): a producer warp (lane 0) walks the CTA's
+// fixed sequence of loads (pass 1 forward, pass 2 backward, row after row) into a ring of S
+// shared-memory stages with cp.async.bulk, and pushes one command per block op; 16 compute
+// warps execute the commands in order; warp 16+1 is idle.  Rows are assigned to clusters
+// round-robin (row = cluster id + k * clusters): no queue, no atomics.
+//
+// Results are bit-identical to the stream and general kernels: the same per-warp pass 1
+// (op_pass1), the same block tree over the 16 warp pairs, the same canonical group / row trees
+// (warp_reduce_leaves over the block values in block order, reading G8), the same pass 2.
+//
+// Deadlock freedom: a CTA's pass 1 of a row depends only on its own loads, whose stages are
+// either released right after the copy to registers or held ones released by pass 2 of the
+// previous row, which (by induction over rows) got its cluster's statistics; so every CTA
+// finishes pass 1 of every row and every row barrier completes.
+#include <cstdlib>
+
+#include "tp_ops.cuh"
+
+namespace tp {
+
+constexpr int kClMaxNb = 256;            // blocks per row (rows of up to 4 Mi elements)
+constexpr int kClMaxLocal = 32;          // blocks per CTA per row (lane of warp 0 per block)
+constexpr int kClThreads = kThreads + 64;
+constexpr int kClCmdSlots = 16;
+constexpr int kClTpSlots = 4;            // pass-1 thread-pair buffers between compute and tree warps
+
+template <typename In> struct ClRing { static constexpr int S = 3; };   // 3 x 64 KB fp32
+template <> struct ClRing<uint16_t> { static constexpr int S = 6; };     // 6 x 32 KB bf16
+
+enum ClOp : int { kClP1 = 0, kClP1Hold = 1, kClP2 = 2, kClP2Held = 3, kClExit = 4 };
+enum ClFlag : int { kClLastP1 = 1, kClFirstP2 = 2 };
+// development counters (KArgs::prof): clock cycles summed over CTAs
+enum ClProf : int {
+    kProfCmdWait = 0, kProfFullWait, kProfRowWait, kProfP1, kProfP2, kProfComputeTotal,
+    kProfFreeStageWait, kProfPushWait, kProfProducerTotal, kProfCtas
+};
+
+struct ClCmd {
+    int op, stage;
+    unsigned parity;  // full[stage] parity of the load (loaded ops)
+    int k;            // row iteration of this cluster (row = cluster id + k * clusters)
+    int li;           // local block index (block = b_lo + li)
+    int flags;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+// shared::cta address -> the same variable's shared::cluster address in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_f2(uint32_t addr, float2 v) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_parity_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ bool wait_cluster_or_abort(uint64_t* bar, uint32_t parity, unsigned* err, unsigned bit) {
+    if (mbar_try_parity_cluster(bar, parity)) return true;
+    const unsigned long long t0 = globaltimer_ns();
+    for (unsigned i = 1;; ++i) {
+        if (mbar_try_parity_cluster(bar, parity)) return true;
+        if ((i & 63u) == 0) {
+            if (*reinterpret_cast<volatile unsigned*>(err)) return false;
+            if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                atomicOr(err, bit);
+                return false;
+            }
+        }
+    }
+}
+
+// Share [b_lo, b_hi) of a row's nb blocks taken by cluster rank r (non-empty when CL <= nb).
+// For row iteration k, CTA q takes share (q + k) mod CL: when CL does not divide nb the larger
+// shares rotate over the CTAs instead of always landing on the same one.
+__device__ __forceinline__ void cl_share(int nb, int CL, int r, int* b_lo, int* nloc) {
+    *b_lo = (r * nb) / CL;
+    *nloc = ((r + 1) * nb) / CL - *b_lo;
+}
+
+// warp_reduce_leaves(kRedPair, n, leaf) for n <= 64, registers only, result in every lane:
+// lane l reduces leaves [l c, l c + c) (c = 2 when next_pow2(n) = 64, else 1), then the warp tree.
+template <typename LeafFn>
+__device__ __forceinline__ Pair warp_tree64(int n, LeafFn leaf) {
+    const int lane = threadIdx.x & 31;
+    Pair v = pair_identity();
+    if (n > 32) {
+        const int b = 2 * lane;
+        if (b < n) v = pair_merge(leaf(b), b + 1 < n ? leaf(b + 1) : pair_identity());
+    } else if (lane < n) {
+        v = leaf(lane);
+    }
+    v = warp_tree_pairs(v);
+    return Pair{__shfl_sync(0xffffffffu, v.m, 0), __shfl_sync(0xffffffffu, v.n, 0)};
+}
+
+// Row statistics from the row's nb block values: the canonical group trees, then the tree over
+// the groups (tp_ops.cuh retire_batch, reading G8), then (n_sum - 1, 0.5 / m_sum) (readings G9,
+// G10).  Every lane gets the result.
+__device__ __forceinline__ float2 cl_row_stats(const float2* vals, int nb) {
+    const int ng = (nb + kGroupBlocks - 1) / kGroupBlocks;
+    const int lane = threadIdx.x & 31;
+    Pair mine = pair_identity();  // lane g keeps group g's value
+#pragma unroll
+    for (int g = 0; g < kClMaxNb / kGroupBlocks; ++g) {
+        if (g < ng) {
+            const float2* base = vals + g * kGroupBlocks;
+            const Pair r = warp_tree64(min(kGroupBlocks, nb - g * kGroupBlocks), [&](int j) {
+                const float2 f = base[j];
+                return Pair{f.x, f.y};
+            });
+            if (lane == g) mine = r;
+        }
+    }
+    Pair root;
+    if (ng > 1) {
+        root = warp_tree_pairs(lane < ng ? mine : pair_identity());
+        root = Pair{__shfl_sync(0xffffffffu, root.m, 0), __shfl_sync(0xffffffffu, root.n, 0)};
+    } else {
+        root = Pair{__shfl_sync(0xffffffffu, mine.m, 0), __shfl_sync(0xffffffffu, mine.n, 0)};
+    }
+    return make_float2(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m));
+}
+
+template <typename In>
+__global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int CL, int H, int J) {
+    constexpr int V = InTraits<In>::V;
+    constexpr int S = ClRing<In>::S;
+    constexpr int C = kClCmdSlots;
+    constexpr int T = kClTpSlots;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ ClCmd cmds[C];
+    __shared__ __align__(16) Pair tpairs[T][kThreads];     // thread pairs of pass-1 blocks
+    __shared__ unsigned char cbits[T][kWarps];            // per-warp clamp decisions of those blocks
+    __shared__ unsigned lmask[2][kClMaxLocal];            // per-block clamp masks, by row parity
+    __shared__ __align__(16) float2 rowvals[2][kClMaxNb];  // written by every CTA of the cluster
+    __shared__ float2 row_st[2];                          // (n_sum - 1, 0.5 / m_sum) of a row
+    __shared__ __align__(8) uint64_t full_bar[S];
+    __shared__ __align__(8) uint64_t empty_bar[S];
+    __shared__ __align__(8) uint64_t cfull_bar[C];
+    __shared__ __align__(8) uint64_t cempty_bar[C];
+    __shared__ __align__(8) uint64_t tp_full[T];           // count 16: thread pairs written
+    __shared__ __align__(8) uint64_t tp_empty[T];          // count 1: read by the tree warp
+    __shared__ __align__(8) uint64_t row_bar[2];           // count CL: one remote arrive per CTA
+    __shared__ __align__(8) uint64_t st_bar[2];            // count 1: row_st written
+
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
+    unsigned* err = &hdr->error;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    In* stages = reinterpret_cast<In*>(dsm);
+    const int nb = (int)a.nb;
+    const int q = (int)cluster_ctarank();
+    const int64_t cid = cluster_id_x(), ncl = nclusters_x();
+    // rows of this cluster: cid, cid + ncl, ...
+    const int K = a.rows > cid ? (int)((a.rows - 1 - cid) / ncl + 1) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kWarps);
+        }
+        for (int c = 0; c < C; ++c) {
+            mbar_init(&cfull_bar[c], 1);
+            mbar_init(&cempty_bar[c], kWarps);
+        }
+        for (int i = 0; i < T; ++i) {
+            mbar_init(&tp_full[i], kWarps);
+            mbar_init(&tp_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&row_bar[i], CL);
+            mbar_init(&st_bar[i], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    cluster_sync_all();  // every CTA's barriers are initialised before any remote arrive
+
+    if (warp == kWarps) {
+        // =============================================================== producer (lane 0)
+        // Command order: P1 of row 0; then for each row k: the first J pass-1 blocks of row k+1
+        // (work for the compute warps while the cluster exchanges row k), pass 2 of row k
+        // (held blocks first, then backwards from L2), the rest of row k+1's pass 1.
+        if (lane != 0) return;
+        const In* x = static_cast<const In*>(a.x);
+        const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+        unsigned use_par = 0, busy = 0;  // bit s: parity of the next use of stage s / stage s in use
+        unsigned held = 0;               // 4 bits per held block of the current row: stage | parity << 3
+        long long pushed = 0;
+        int rr = 0;
+        bool ok = true;
+        unsigned long long pc_free = 0, pc_push = 0;
+        const unsigned long long pc_start = clock64();
+
+        auto push = [&](ClCmd cmd) {
+            const int c = (int)(pushed % C);
+            const unsigned long long t0 = clock64();
+            if (pushed >= C && !wait_or_abort(&cempty_bar[c], (uint32_t)(((pushed / C) - 1) & 1), err, 64u)) {
+                ok = false;
+                return;
+            }
+            pc_push += clock64() - t0;
+            cmds[c] = cmd;
+            mbar_arrive(&cfull_bar[c]);
+            ++pushed;
+        };
+        // a free stage (its previous use fully read), round robin
+        auto free_stage = [&]() -> int {
+            const unsigned long long t0 = globaltimer_ns();
+            const unsigned long long c0 = clock64();
+            for (unsigned i = 0;; ++i) {
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    int s = rr + j;
+                    s = s >= S ? s - S : s;
+                    if (((busy >> s) & 1u) && mbar_test_parity(&empty_bar[s], ((use_par >> s) & 1u) ^ 1u))
+                        busy &= ~(1u << s);
+                    if (!((busy >> s) & 1u)) {
+                        rr = s + 1 == S ? 0 : s + 1;
+                        pc_free += clock64() - c0;
+                        return s;
+                    }
+                }
+                if ((i & 63u) == 63u) {
+                    if (aborted(err)) return -1;
+                    if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                        atomicOr(err, 128u);
+                        return -1;
+                    }
+                }
+            }
+        };
+        auto load = [&](int s, int64_t row, int blk, uint64_t pol) -> unsigned {
+            const int64_t e0 = (int64_t)blk * kBlockElems;
+            const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
+            const unsigned parity = (use_par >> s) & 1u;
+            use_par ^= 1u << s;
+            busy |= 1u << s;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], bytes);
+            tma_load_1d(stages + (size_t)s * kBlockElems, x + row * a.cols + e0, bytes, &full_bar[s], pol);
+            return parity;
+        };
+        auto p1 = [&](int k, int li0, int li1) {  // pass-1 blocks [li0, li1) of row iteration k
+            int b_lo, nloc;
+            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
+            const int hold = min(H, nloc);
+            const int64_t row = cid + (int64_t)k * ncl;
+            for (int li = li0; li < li1 && ok; ++li) {
+                const bool h = li >= nloc - hold;
+                const int s = free_stage();
+                if (s < 0) { ok = false; break; }
+                const unsigned par = load(s, row, b_lo + li, h ? pol_drop : pol_keep);
+                if (h) {
+                    const int hi = li - (nloc - hold);
+                    held = (held & ~(0xfu << (4 * hi))) | ((unsigned)(s | (par << 3)) << (4 * hi));
+                }
+                push(ClCmd{h ? kClP1Hold : kClP1, s, par, k, b_lo + li, 0});
+            }
+        };
+        auto p2 = [&](int k) {  // pass 2 of row iteration k, backwards
+            int b_lo, nloc;
+            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
+            const int hold = min(H, nloc);
+            const int64_t row = cid + (int64_t)k * ncl;
+            for (int li = nloc - 1; li >= 0 && ok; --li) {
+                const int fl = li == nloc - 1 ? kClFirstP2 : 0;
+                if (li >= nloc - hold) {
+                    const unsigned hs = (held >> (4 * (li - (nloc - hold)))) & 0xfu;
+                    push(ClCmd{kClP2Held, (int)(hs & 7u), hs >> 3, k, b_lo + li, fl | (li << 8)});
+                } else {
+                    const int s = free_stage();
+                    if (s < 0) { ok = false; break; }
+                    const unsigned par = load(s, row, b_lo + li, pol_drop);
+                    push(ClCmd{kClP2, s, par, k, b_lo + li, fl | (li << 8)});
+                }
+            }
+        };
+        auto nloc_of = [&](int k) {
+            int b_lo, nloc;
+            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
+            return nloc;
+        };
+
+        if (K > 0) p1(0, 0, nloc_of(0));
+        for (int k = 0; k < K && ok; ++k) {
+            int j = 0;
+            if (k + 1 < K) {  // look-ahead blocks are never held ones
+                const int n1 = nloc_of(k + 1);
+                j = max(0, min(J, n1 - min(H, n1)));
+                p1(k + 1, 0, j);
+            }
+            p2(k);
+            if (k + 1 < K) p1(k + 1, j, nloc_of(k + 1));
+        }
+        if (ok) push(ClCmd{kClExit, 0, 0, 0, 0, 0});
+        if (a.prof) {
+            atomicAdd(&a.prof[kProfFreeStageWait], pc_free);
+            atomicAdd(&a.prof[kProfPushWait], pc_push);
+            atomicAdd(&a.prof[kProfProducerTotal], clock64() - pc_start);
+            atomicAdd(&a.prof[kProfCtas], 1ull);
+        }
+        return;
+    }
+    if (warp > kWarps) {
+        // =============================================================== tree warp
+        // Per pass-1 block, in command order: the perfect tree over the 512 thread pairs in
+        // thread order (lane l reduces threads 16l..16l+15, then the warp tree) = the stream
+        // kernel's warp trees followed by its block tree over the 16 warps (reading G8).  After
+        // a row's last local block: block values to every CTA of the cluster, then the row
+        // statistics for this CTA's compute warps.
+        long long p = 0;
+        for (int k = 0; k < K; ++k) {
+            const int par = k & 1;
+            int b_lo, nloc;
+            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
+            float2 lval = make_float2(0.f, 0.f);  // lane li: value of local block li
+            unsigned lm = 0;
+            bool ok = true;
+            for (int li = 0; li < nloc; ++li, ++p) {
+                const int sl = (int)(p % T);
+                if (!wait_or_abort(&tp_full[sl], (uint32_t)((p / T) & 1), err, 512u)) { ok = false; break; }
+                const Pair* tq = tpairs[sl] + lane * 16;
+                const Pair t = tree_pairs_n<16>([&](int i) { return tq[i]; });
+                unsigned m = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) m |= (unsigned)cbits[sl][w] << w;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tp_empty[sl]);
+                const Pair b = warp_tree_pairs(t);  // lane 0
+                const float bm = __shfl_sync(0xffffffffu, b.m, 0), bn = __shfl_sync(0xffffffffu, b.n, 0);
+                if (lane == li) {
+                    lval = make_float2(bm, bn);
+                    lm = m;
+                }
+            }
+            if (!ok) break;
+            if (lane < nloc) {
+                lmask[par][lane] = lm;
+                const uint32_t dst = smem_u32(&rowvals[par][b_lo + lane]);
+                for (int r = 0; r < CL; ++r) st_cluster_f2(mapa(dst, (uint32_t)r), lval);
+            }
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            __syncwarp();
+            if (lane < CL) mbar_arrive_remote(mapa(smem_u32(&row_bar[par]), (uint32_t)lane));
+            if (!wait_cluster_or_abort(&row_bar[par], (uint32_t)((k >> 1) & 1), err, 256u)) break;
+            const float2 st = cl_row_stats(rowvals[par], nb);
+            if (lane == 0) {
+                row_st[par] = st;
+                mbar_arrive(&st_bar[par]);
+            }
+        }
+        return;
+    }
+
+    // =================================================================== compute warps
+    float2 st = make_float2(0.f, 0.f);
+    long long np1 = 0;  // pass-1 blocks handed to the tree warp
+    unsigned long long pc[kProfComputeTotal] = {0, 0, 0, 0, 0};
+    const unsigned long long pc_start = clock64();
+    unsigned long long tq = pc_start;
+    auto lap = [&](int slot) {
+        const unsigned long long t = clock64();
+        pc[slot] += t - tq;
+        tq = t;
+    };
+    for (long long c = 0;; ++c) {
+        const int cs = (int)(c % C);
+        tq = clock64();
+        if (!wait_or_abort(&cfull_bar[cs], (uint32_t)((c / C) & 1), err, 8u)) break;
+        lap(kProfCmdWait);
+        const ClCmd cmd = cmds[cs];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty_bar[cs]);
+        if (cmd.op == kClExit) break;
+        const int64_t row = cid + (int64_t)cmd.k * ncl;
+        const int blk = cmd.li;  // absolute block index
+        const int valid = (int)min((int64_t)kBlockElems, a.cols - (int64_t)blk * kBlockElems);
+        const int par = cmd.k & 1;
+        In* stage = stages + (size_t)cmd.stage * kBlockElems;
+        BlockVals v;
+        if (cmd.op == kClP1 || cmd.op == kClP1Hold) {
+            if (!wait_or_abort(&full_bar[cmd.stage], cmd.parity, err, 4u)) break;
+            lap(kProfFullWait);
+            load_stage<In>(stage, v);
+            if (cmd.op == kClP1) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[cmd.stage]);
+            }
+            bool cl;
+            const Pair tp_ = thread_pass1<V>(v, valid, &cl);
+            const int sl = (int)(np1 % T);
+            if (np1 >= T && !wait_or_abort(&tp_empty[sl], (uint32_t)(((np1 / T) - 1) & 1), err, 1024u)) break;
+            ++np1;
+            tpairs[sl][threadIdx.x] = tp_;
+            if (lane == 0) cbits[sl][warp] = cl ? 1 : 0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tp_full[sl]);
+            lap(kProfP1);
+        } else {
+            if (cmd.flags & kClFirstP2) {  // the row's statistics, from the tree warp
+                if (!wait_or_abort(&st_bar[par], (uint32_t)((cmd.k >> 1) & 1), err, 256u)) break;
+                st = row_st[par];
+                lap(kProfRowWait);
+            }
+            if (cmd.op == kClP2 && !wait_or_abort(&full_bar[cmd.stage], cmd.parity, err, 4u)) break;
+            lap(kProfFullWait);
+            load_stage<In>(stage, v);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[cmd.stage]);
+            const bool my_clamp = ((lmask[par][cmd.flags >> 8] >> warp) & 1u) != 0;
+            op_pass2<V>(v, make_float4(st.x, st.y, 0.f, 0.f), my_clamp, a.y + row * a.cols + (int64_t)blk * kBlockElems,
+                        valid, true);
+            lap(kProfP2);
+        }
+    }
+    if (a.prof && warp == 0 && lane == 0) {
+        for (int i = 0; i < kProfComputeTotal; ++i) atomicAdd(&a.prof[i], pc[i]);
+        atomicAdd(&a.prof[kProfComputeTotal], clock64() - pc_start);
+    }
+}
+
+// ----------------------------------------------------------------------------- host side
+template <typename In>
+static int max_active_clusters(int dev, int CL, size_t dyn) {
+    static int cache[64][4];
+    const int ci = CL == 1 ? 0 : CL == 2 ? 1 : CL == 4 ? 2 : 3;
+    if (cache[dev][ci]) return cache[dev][ci] > 0 ? cache[dev][ci] : 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(CL * 8));
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = dyn;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, rowcl_kernel<In>, &cfg) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = -1;
+    }
+    cache[dev][ci] = n;
+    return n > 0 ? n : 0;
+}
+
+template <typename In>
+static size_t rowcl_dyn_smem() {
+    return (size_t)ClRing<In>::S * kBlockElems * sizeof(In);
+}
+
+template <typename In>
+static void rowcl_configure(int dev) {
+    static int configured[64];
+    if (!configured[dev]) {
+        cudaFuncSetAttribute(rowcl_kernel<In>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
+        configured[dev] = 1;
+    }
+}
+
+// Cluster size for a launch, or 0 when the stream schedule is the better choice.  Estimated
+// time ~ rounds x (blocks per CTA + 1 for the row exchange); the L2 working set (pass-1 blocks
+// waiting for their pass-2 re-read, about half a row per cluster) must stay well inside L2.
+template <typename In>
+int rowcl_choose(int64_t rows, int64_t nb, int force_cl) {
+    if (nb < 2 || nb > kClMaxNb) return 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    rowcl_configure<In>(dev);
+    const size_t dyn = rowcl_dyn_smem<In>();
+    const double block_bytes = (double)kBlockElems * sizeof(In);
+    const int H = ClRing<In>::S - 1;
+    int best = 0;
+    double best_t = 0.0;
+    for (int CL = 1; CL <= 8; CL *= 2) {
+        if (CL > nb || (nb + CL - 1) / CL > kClMaxLocal) continue;
+        if (force_cl && CL != force_cl) continue;
+        const int Q = max_active_clusters<In>(dev, CL, dyn);
+        if (Q < 1) continue;
+        const int64_t active = rows < Q ? rows : Q;
+        const int64_t rounds = (rows + Q - 1) / Q;
+        const int64_t per_cta = (nb + CL - 1) / CL;
+        const double t = (double)rounds * ((double)per_cta + 1.0);
+        const double resident = (double)active * (double)(nb - (int64_t)CL * H > 0 ? nb - (int64_t)CL * H : 0) *
+                                block_bytes * 0.5;
+        if (!force_cl && resident > 64e6) continue;
+        if (best == 0 || t < best_t) best = CL, best_t = t;
+    }
+    return best;
+}
+
+template <typename In>
+cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    rowcl_configure<In>(dev);
+    const size_t dyn = rowcl_dyn_smem<In>();
+    int Q = max_active_clusters<In>(dev, CL, dyn);
+    if (Q < 1) return cudaErrorInvalidConfiguration;
+    if (o.grid_ctas > 0 && o.grid_ctas / CL < Q) Q = (int)(o.grid_ctas / CL > 0 ? o.grid_ctas / CL : 1);
+    const int64_t ncl = a.rows < Q ? a.rows : Q;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(ncl * CL));
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static const int env_h = [] {
+        const char* e = getenv("TP_CL_HOLD");
+        return e ? atoi(e) : -1;
+    }();
+    static const int env_j = [] {
+        const char* e = getenv("TP_CL_LOOKAHEAD");
+        return e ? atoi(e) : -1;
+    }();
+    const int H = env_h >= 0 ? min(env_h, ClRing<In>::S - 1) : ClRing<In>::S - 1;
+    const int J = env_j >= 0 ? min(env_j, kClTpSlots - 1) : 2;
+    last_plan() = Plan{3, kTwoPass, ncl * CL, CL, J, H};
+    return cudaLaunchKernelEx(&cfg, rowcl_kernel<In>, a, CL, H, J);
+}
+
+template int rowcl_choose<float>(int64_t, int64_t, int);
+template int rowcl_choose<uint16_t>(int64_t, int64_t, int);
+template cudaError_t launch_rowcl<float>(KArgs, int, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_rowcl<uint16_t>(KArgs, int, const LaunchOpts&, cudaStream_t);
+
+}  // namespace tp

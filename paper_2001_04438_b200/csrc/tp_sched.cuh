@@ -60,6 +60,7 @@ struct KArgs {
     int vec;                 // 16-byte aligned rows
     int l2_hints;            // TMA loads carry evict_last / evict_first L2 policies
     int hold;                // stream kernel: blocks stay staged between pass 1 and pass 2
+    unsigned long long* prof;  // development: per-role cycle counters (tp_set_profile_buffer), or null
 };
 
 // number of (phase, row) units in schedule slots < s.  Item arithmetic is 32-bit: a launch
@@ -98,7 +99,8 @@ __device__ __forceinline__ Item decode_item(int64_t item64, int64_t R64, int64_t
         if (units_before(mid, R, L, P) <= unit) lo = mid; else hi = mid;
     }
     const uint32_t s = lo;
-    const int p_hi = (int)((s / L) < (uint32_t)(P - 1) ? (s / L) : (uint32_t)(P - 1));
+    const uint32_t pmax = (uint32_t)(P - 1);
+    const int p_hi = (int)(s / L < pmax ? s / L : pmax);
     const uint32_t idx = unit - units_before(s, R, L, P);
     it.phase = p_hi - (int)idx;  // within a slot: oldest row (highest phase) first
     it.row = s - (uint32_t)it.phase * L;

@@ -406,6 +406,7 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     // stream mode: items a CTA holds between hand-out and retirement (its stages, the prefetched
     // queue chunks and the part-slot backlog; measured: C4 gains up to L ~ 50 rows)
     a.L = lookahead_rows(a, grid, S + 12, o);
+    last_plan() = Plan{2, A, grid, 0, a.L, a.hold};
     kern<<<(unsigned)grid, kStreamThreads, dyn, s>>>(a);
     return cudaGetLastError();
 }

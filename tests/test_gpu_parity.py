@@ -231,6 +231,44 @@ def test_hold_and_reread_schedules_agree_bitwise(rows, cols, dtype):
         assert_parity(x, a, "hold")
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", [(64, 32768), (5, 16384 + 4), (9, 16384 * 5 + 12), (40, 800000),
+                                       (3, 16384 * 64), (2, 16384 * 100 + 8), (2, 16384 * 256),
+                                       (1, 16384 * 257), (300, 16384 * 2 + 100)])
+def test_cluster_schedule_agrees_bitwise_with_stream(rows, cols, dtype):
+    # cluster: one thread-block cluster per row, block values exchanged through DSMEM, pass 2
+    # from shared memory / L2 (tp_rowcl.cu); stream: the row spread over the persistent grid.
+    # Same canonical trees (reading G8), so the outputs must be bit-identical; 2..256 blocks
+    # per row use the cluster kernel (nb = 257 falls back to the stream kernel).
+    x = workloads.ragged_case(rows, cols, -500, 500, seed=8, stream=cols + rows)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    for cl in [0, 1, 2, 4, 8]:
+        y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_CLUSTER, cluster_size=cl))
+        assert tp.watchdog_flags() == 0
+        assert np.array_equal(ref, y), (cl, rows, cols)
+    assert np.array_equal(ref, to_host(tp.softmax(xd)))
+    if rows * cols <= 3_000_000:
+        assert_parity(x, ref, "cluster")
+
+
+def test_cluster_schedule_clamped_blocks_and_small_grids():
+    # out-of-domain blocks (reading G11) inside multi-block rows: the per-warp clamp masks stay
+    # local to the CTA that ran pass 1; a capped grid makes clusters loop over many rows
+    x = workloads.ragged_case(24, 16384 * 6 + 40, -50, 50, seed=9, stream=9)
+    x[1, 100] = 3.0e7
+    x[5, 16384 * 3 + 7] = -1.0e9
+    x[7, :] = -5.0e6
+    xd = to_dev(x)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    for cl, g in [(2, 2), (4, 8), (1, 1), (8, 0)]:
+        y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_CLUSTER, cluster_size=cl, grid_ctas=g))
+        assert np.array_equal(ref, y), (cl, g)
+    assert np.isfinite(ref).all()
+
+
 def test_out_of_domain_blocks_take_the_clamped_path():
     # a row with one huge element, a row entirely below -2^21, a row with +-inf/NaN-free extremes:
     # outputs finite, non-negative, summing to 1; in-domain rows unaffected (reading G11)

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--no-tma", action="store_true")
     ap.add_argument("--lookahead", type=int, default=0)
+    ap.add_argument("--schedule", type=int, default=0)
+    ap.add_argument("--cluster-size", type=int, default=0)
     args = ap.parse_args()
     x = workloads.generate(args.config, nrows=args.rows)
     if x.dtype == np.uint16:
@@ -35,11 +37,12 @@ def main():
         xd = torch.from_numpy(x).cuda()
     y = torch.empty(xd.shape, dtype=torch.float32, device="cuda")
     for _ in range(args.iters):
-        tp.softmax_ex(xd, ALGO[args.algo], out=y, disable_tma=args.no_tma, lookahead_rows=args.lookahead)
+        tp.softmax_ex(xd, ALGO[args.algo], out=y, disable_tma=args.no_tma, lookahead_rows=args.lookahead,
+                      schedule=args.schedule, cluster_size=args.cluster_size)
     torch.cuda.synchronize()
     assert tp.watchdog_flags() == 0
     assert bool(torch.isfinite(y).all())
-    print("ok", args.config, args.algo, tuple(xd.shape))
+    print("ok", args.config, args.algo, tuple(xd.shape), tp.last_plan())
 
 
 if __name__ == "__main__":

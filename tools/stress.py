@@ -54,7 +54,7 @@ def main():
                 bad.append((i, f, ts[-1]))
         ts = np.array(ts)
         print(json.dumps(dict(spec=spec, median_us=float(np.median(ts)), min_us=float(ts.min()),
-                              max_us=float(ts.max()), p90_us=float(np.percentile(ts, 90)), n_bad=len(bad),
+                              max_us=float(ts.max()), p90_us=float(np.percentile(ts, 90)), n_bad=len(bad), plan=tp.last_plan(),
                               bad=bad[:10])), flush=True)
 
 
