@@ -202,12 +202,19 @@ def cpu_baseline(args, spec):
 
 # ---------------------------------------------------------------- our arm
 
-def traffic_from_profiles(workload: str):
+KERNEL_NAMES = {"stream": "tp::stream_kernel<{In},kTwoPass>", "cluster": "tp::rowcl_kernel<{In}>",
+                "general": "tp::general_kernel<{In},kTwoPass>"}
+
+
+def traffic_from_profiles(workload: str, kernel: str):
+    """DRAM bytes per launch of this workload's kernel from the committed ncu capture, else None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p)).get(workload)
-    return None if d is None else d.get("dram_bytes_per_launch")
+    if d is None or d.get("kernel") != kernel:
+        return None
+    return d.get("dram_bytes_per_launch")
 
 
 def main():
@@ -307,6 +314,8 @@ def main():
         return float(t.item()), per_launch, clocks
 
     total_ms, per_launch_ms, clocks = timed(step_two_pass, args.steps, args.warmup, sample_clocks=True)
+    plan = tp.last_plan()  # which kernel the timed launches ran
+    kernel_name = KERNEL_NAMES.get(plan["kernel"], plan["kernel"]).format(In="float" if dtype == "f32" else "uint16_t")
     if tp.watchdog_flags(ws, reset=True):
         raise RuntimeError("watchdog fired during the benchmark: results invalid")
 
@@ -329,6 +338,13 @@ def main():
                          "GBps_own_cost_model": BYTES_PER_ELEM[(nm, dtype)] * elems_total / (ms * 1e-3) / 1e9,
                          "GBps_at_two_pass_bytes": value * ms_per_step / ms,
                          "two_pass_speedup": ms / ms_per_step}
+        if plan["kernel"] == "cluster":  # the same Two-Pass on the grid-wide stream schedule, for context
+            tot, _, _ = timed(lambda: tp.softmax_ex(x, tp.ALGO_TWO_PASS, out=y, workspace=ws,
+                                                    schedule=tp.SCHED_STREAM), args.steps, args.warmup)
+            ms = tot / args.steps
+            three["two_pass_stream_schedule"] = {"ms_per_step": ms,
+                                                 "GBps": per_elem * elems_total / (ms * 1e-3) / 1e9,
+                                                 "cluster_schedule_speedup": ms / ms_per_step}
 
     # end to end through the C ABI on host (pinned) buffers: H2D + kernels + D2H every step
     e2e = None
@@ -366,9 +382,8 @@ def main():
             "elements_per_s": elems_total / (ms_per_step * 1e-3),
             "pct_of_8TBs": value / world / NOMINAL_HBM_GBS if spec["scaling"] == "weak" else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload),
-                         "kernel": "tp::stream_kernel<float,kTwoPass>" if dtype == "f32" else
-                                   "tp::stream_kernel<uint16_t,kTwoPass>",
+                         "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload, kernel_name),
+                         "kernel": kernel_name, "plan": plan,
                          "algorithmic_bytes_per_launch": per_elem * n_local,
                          "launch_ms_mean": launch_ms, "peak_source": peak_src},
             "three_pass": three or None,

@@ -175,7 +175,10 @@ int tp_debug_op(int what, const float* a, const float* b, float* out0, float* ou
 /* Compute-only throughput probe (roofline evidence, not part of the method): `ctas` CTAs of
  * 512 threads each run `reps` times over one shared-memory block of 16384 synthetic logits:
  * what = 0 pass 1, 1 pass 2 (no store), 2 both; 3-6 instruction throughput (64 per thread
- * per rep: 3 FFMA2, 4 FFMA2 with an immediate, 5 FFMA, 6 integer add-max + shift).  sink: device, ctas*16 floats (results are
+ * per rep: 3 FFMA2, 4 FFMA2 with an immediate, 5 FFMA, 6 integer add-max + shift); 7 pass 1
+ * without the warp tree; 8 pass 2 with its stores, 9 the stores alone, 10 the stores through
+ * shared memory and one bulk (TMA) store per block, 11 the stores as 256-bit vectors (8-11: sink
+ * needs ctas*16 + ctas*16384 floats).  sink: device, ctas*16 floats (results are
  * meaningless; they keep the work alive).  in_dtype TP_IN_F32 / TP_IN_BF16. */
 /* Development: a device buffer of 16 uint64 counters (zeroed by the caller) that later
  * cluster-kernel launches accumulate per-role clock cycles into, summed over CTAs

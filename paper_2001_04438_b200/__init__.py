@@ -20,7 +20,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_PKG, "libtwopass.so")
+# TP_LIBRARY: development override (an alternative in-tree build of the same library)
+_SO = os.environ.get("TP_LIBRARY") or os.path.join(_PKG, "libtwopass.so")
 
 TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV = 0, 1, 2, 3
 ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3

@@ -28,10 +28,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines: tuple = ()) -> str:
+    if not force and out == SO and not _stale():
         return SO
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", SO,
+    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines], "-o", out,
            *[os.path.join(CSRC, f) for f in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -39,7 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libtwopass.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    return SO
+    return out
 
 
 if __name__ == "__main__":

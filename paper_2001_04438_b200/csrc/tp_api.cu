@@ -421,7 +421,7 @@ int tp_set_profile_buffer(void* p) {
 }
 
 int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink, cudaStream_t stream) {
-    if (what < 0 || what > 9 || ctas < 1 || reps < 1 || !sink || (in_dtype != TP_IN_F32 && in_dtype != TP_IN_BF16))
+    if (what < 0 || what > 11 || ctas < 1 || reps < 1 || !sink || (in_dtype != TP_IN_F32 && in_dtype != TP_IN_BF16))
         return TP_EINVAL;
     cudaError_t e = tp::launch_bench_compute(what, in_dtype == TP_IN_BF16, ctas, reps, sink, stream);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);

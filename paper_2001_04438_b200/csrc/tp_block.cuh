@@ -98,6 +98,17 @@ __device__ __forceinline__ void load_global_y(const float* yb, int valid, bool v
 template <int V>
 __device__ __forceinline__ void store_block(float* yb, int valid, bool vec, const BlockVals& r) {
     constexpr int NV = kPerThread / V;
+    if (vec && valid == kBlockElems) {  // whole block: unconditional 128-bit stores
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int e = V * ((int)threadIdx.x + kThreads * k);
+#pragma unroll
+            for (int h = 0; h < V; h += 4)
+                st_cs_f4(yb + e + h, make_float4(r.v[k * V + h], r.v[k * V + h + 1], r.v[k * V + h + 2],
+                                                 r.v[k * V + h + 3]));
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
         const int e = V * ((int)threadIdx.x + kThreads * k);
@@ -135,87 +146,69 @@ __device__ __forceinline__ Pair pass1_thread(const BlockVals& r, int valid) {
     return accv_pair(acc);
 }
 
-// Variant: the thread's largest exponent first (one FFMA2 per pair), then every element scaled
-// to it and summed into 4 independent accumulators (no serial rescaling chain).
-template <int V, bool FULL, bool CLAMP>
-__device__ __forceinline__ Pair pass1_thread_v2(const BlockVals& r, int valid) {
-    float vmax = 0.0f;
-#pragma unroll
-    for (int i = 0; i < kPerThread; i += 2) {
-        float2 x = make_float2(r.v[i], r.v[i + 1]);
-        if (CLAMP) {
-            x.x = fminf(fmaxf(x.x, -kXClamp), kXClamp);
-            x.y = fminf(fmaxf(x.y, -kXClamp), kXClamp);
-        }
-        float2 v = ffma2(x, bc2(kLog2e), bc2(kMagic));
-        if (!FULL) {
-            if (!(elem_off<V>(i) < valid)) v.x = 0.0f;
-            if (!(elem_off<V>(i + 1) < valid)) v.y = 0.0f;
-        }
-        vmax = fmaxf(vmax, fmaxf(v.x, v.y));
-    }
-    const int c = __float_as_int(vmax) - 127;
-    float2 s[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-    for (int i = 0; i < kPerThread; i += 2) {
-        float2 m, v;
-        ext_exp2v<CLAMP>(make_float2(r.v[i], r.v[i + 1]), m, v);
-        if (!FULL) {
-            if (!(elem_off<V>(i) < valid)) { m.x = 0.0f; v.x = 0.0f; }
-            if (!(elem_off<V>(i + 1) < valid)) { m.y = 0.0f; v.y = 0.0f; }
-        }
-        const int j = (i / 2) & 3;
-        s[j] = ffma2(m, make_float2(pow2_bits(__float_as_int(v.x) - c), pow2_bits(__float_as_int(v.y) - c)), s[j]);
-    }
-    const float2 t = fadd2(fadd2(s[0], s[1]), fadd2(s[2], s[3]));
-    const float n = vmax != 0.0f ? __fsub_rn(vmax, kMagic) : -kFltMax;
-    return Pair{__fadd_rn(t.x, t.y), n};
+// Pass 2: y = (m * lambda') * 2^(n - (n_sum - 1)), lambda' = 0.5 / m_sum (PAPER.md:166-168 with
+// reading G9: never form lambda * 2^k first).  m lambda' = lambda' p(t) is evaluated with the
+// coefficients lambda' c_i (one rounding each, once per block): a multiply less per element, and
+// p(0) lambda' = lambda' exactly.  2^(n - nsum1) = pow2_bits(bits(v) - c), flushed to 0 below
+// 2^-126; |nsum1| <= 3025526 (reading G11) is exactly an int.
+struct Pass2Consts {
+    int c;
+    float l1, l2, l3, l4, l5, l0;
+};
+__device__ __forceinline__ Pass2Consts pass2_consts(float nsum1, float lam_half) {
+    return Pass2Consts{magic_bits() + __float2int_rn(nsum1) - 127, __fmul_rn(lam_half, kC1),
+                       __fmul_rn(lam_half, kC2), __fmul_rn(lam_half, kC3), __fmul_rn(lam_half, kC4),
+                       __fmul_rn(lam_half, kC5), lam_half};
 }
 
-// Pass 2 variant with lambda' folded into the polynomial (coefficients lambda' c_i, per call).
 template <bool CLAMP>
-__device__ __forceinline__ void pass2_thread_v2(BlockVals& r, float nsum1, float lam_half) {
-    const int c = magic_bits() + __float2int_rn(nsum1) - 127;
-    const float l1 = __fmul_rn(lam_half, kC1), l2 = __fmul_rn(lam_half, kC2), l3 = __fmul_rn(lam_half, kC3),
-                l4 = __fmul_rn(lam_half, kC4), l5 = __fmul_rn(lam_half, kC5);
-#pragma unroll
-    for (int i = 0; i < kPerThread; i += 2) {
-        float2 x = make_float2(r.v[i], r.v[i + 1]);
-        if (CLAMP) {
-            x.x = fminf(fmaxf(x.x, -kXClamp), kXClamp);
-            x.y = fminf(fmaxf(x.y, -kXClamp), kXClamp);
-        }
-        const float2 v = ffma2(x, bc2(kLog2e), bc2(kMagic));
-        const float2 n = fadd2(v, bc2(-kMagic));
-        float2 t = ffma2(n, bc2(-kLn2Hi), x);
-        t = ffma2(n, bc2(-kLn2Lo), t);
-        float2 p = ffma2(bc2(l5), t, bc2(l4));
-        p = ffma2(p, t, bc2(l3));
-        p = ffma2(p, t, bc2(l2));
-        p = ffma2(p, t, bc2(l1));
-        p = ffma2(p, t, bc2(lam_half));
-        const float2 s = make_float2(pow2_bits(__float_as_int(v.x) - c), pow2_bits(__float_as_int(v.y) - c));
-        const float2 y = fmul2(p, s);
-        r.v[i] = y.x;
-        r.v[i + 1] = y.y;
+__device__ __forceinline__ float2 pass2_pair(float2 x, const Pass2Consts& k) {
+    if (CLAMP) {
+        x.x = fminf(fmaxf(x.x, -kXClamp), kXClamp);
+        x.y = fminf(fmaxf(x.y, -kXClamp), kXClamp);
     }
+    const float2 v = ffma2(x, bc2(kLog2e), bc2(kMagic));  // ExtExp
+    const float2 n = fadd2(v, bc2(-kMagic));
+    float2 t = ffma2(n, bc2(-kLn2Hi), x);
+    t = ffma2(n, bc2(-kLn2Lo), t);
+    float2 p = ffma2(bc2(k.l5), t, bc2(k.l4));
+    p = ffma2(p, t, bc2(k.l3));
+    p = ffma2(p, t, bc2(k.l2));
+    p = ffma2(p, t, bc2(k.l1));
+    p = ffma2(p, t, bc2(k.l0));
+    const float2 s = make_float2(pow2_bits(__float_as_int(v.x) - k.c), pow2_bits(__float_as_int(v.y) - k.c));
+    return fmul2(p, s);
 }
 
-// Pass 2 in place: y = (m * lambda') * 2^(n - (n_sum - 1)), lambda' = 0.5 / m_sum
-// (PAPER.md:166-168 with reading G9: never form lambda * 2^k first).
+// In place on this thread's values.
 template <bool CLAMP>
 __device__ __forceinline__ void pass2_thread(BlockVals& r, float nsum1, float lam_half) {
-    // 2^(n - nsum1) = pow2_bits(bits(v) - c), flushed to 0 below 2^-126 (reading G9);
-    // |nsum1| <= 3025526 (reading G11), exactly an int
-    const int c = magic_bits() + __float2int_rn(nsum1) - 127;
+    const Pass2Consts k = pass2_consts(nsum1, lam_half);
 #pragma unroll
     for (int i = 0; i < kPerThread; i += 2) {
-        float2 m, v;
-        ext_exp2v<CLAMP>(make_float2(r.v[i], r.v[i + 1]), m, v);
-        const float2 s = make_float2(pow2_bits(__float_as_int(v.x) - c), pow2_bits(__float_as_int(v.y) - c));
-        const float2 y = fmul2(fmul2(m, bc2(lam_half)), s);
+        const float2 y = pass2_pair<CLAMP>(make_float2(r.v[i], r.v[i + 1]), k);
         r.v[i] = y.x;
         r.v[i + 1] = y.y;
+    }
+}
+
+// Whole 16-byte aligned block: each vector's outputs stored as soon as they are computed, so
+// the stores overlap the arithmetic of the next vectors.
+template <int V, bool CLAMP>
+__device__ __forceinline__ void pass2_store_full(const BlockVals& r, float nsum1, float lam_half, float* yb) {
+    const Pass2Consts k = pass2_consts(nsum1, lam_half);
+#pragma unroll
+    for (int j = 0; j < kPerThread / V; ++j) {
+        float o[V];
+#pragma unroll
+        for (int q = 0; q < V; q += 2) {
+            const float2 y = pass2_pair<CLAMP>(make_float2(r.v[j * V + q], r.v[j * V + q + 1]), k);
+            o[q] = y.x;
+            o[q + 1] = y.y;
+        }
+        const int e = V * ((int)threadIdx.x + kThreads * j);
+#pragma unroll
+        for (int h = 0; h < V; h += 4) st_cs_f4(yb + e + h, make_float4(o[h], o[h + 1], o[h + 2], o[h + 3]));
     }
 }
 

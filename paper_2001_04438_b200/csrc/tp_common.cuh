@@ -130,7 +130,10 @@ __device__ __forceinline__ void ext_exp2v(float2 x, float2& m, float2& v) {
 // 2^(d - 127) for an integer d <= 255, flushed to +0 for d <= 0: the value ex2_ftz gives for the
 // integer exponent d - 127 (reading G5), built in the exponent field on the integer pipe
 // (no MUFU): max, shift.  With d = bits(v) - c this is 2^(n - (c - bits(1.5*2^23) + 127)).
-__device__ __forceinline__ float pow2_bits(int d) { return __int_as_float(max(d, 0) << 23); }
+__device__ __forceinline__ float pow2_bits(int d) {
+    // funnel shift: SHF on the integer pipe (a plain << compiles to IMAD.SHL on the FMA pipe)
+    return __int_as_float((int)__funnelshift_l(0u, (unsigned)max(d, 0), 23));
+}
 __device__ __forceinline__ int magic_bits() { return __float_as_int(kMagic); }
 
 // Exp with reconstruction for the Three-Pass comparators (Alg. 4), argument
@@ -401,7 +404,26 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 // streaming (evict-first) 128-bit store of outputs that are not re-read
-__device__ __forceinline__ void st_cs_f4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
+#ifndef TP_STORE_MODE
+#define TP_STORE_MODE 0
+#endif
+__device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
+#if TP_STORE_MODE == 0
+    __stcs(reinterpret_cast<float4*>(p), v);
+#elif TP_STORE_MODE == 1
+    *reinterpret_cast<float4*>(p) = v;
+#else
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+#endif
+}
+
+// 256-bit store of 8 consecutive floats (STG.E.ENL2.256 on sm_100a), evict-first
+__device__ __forceinline__ void st_cs_f8(float* p, const float* v) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                 "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
 
 // bf16 bits -> fp32: exact 16-bit left shift
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -484,6 +506,23 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
             smem_u32(smem_dst)),
         "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+
+// shared -> global bulk copy (TMA store), tracked by this thread's bulk async-groups
+__device__ __forceinline__ void tma_store_1d(void* gmem_dst, const void* smem_src, uint32_t bytes, uint64_t policy) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem_dst),
+                 "r"(smem_u32(smem_src)), "r"(bytes), "l"(policy)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N of this thread's committed bulk groups still reading shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_1d_nohint(void* smem_dst, const void* gmem_src, uint32_t bytes,

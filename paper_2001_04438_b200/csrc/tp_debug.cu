@@ -75,16 +75,44 @@ __global__ void __launch_bounds__(kThreads, 1) bench_compute_kernel(int what, in
             v.v[i] = t.x;
             v.v[i + 1] = t.y;
         }
-        if (what == 7) {
-            acc += pass1_thread_v2<V, true, false>(v, kBlockElems).m;
-        } else if (what == 8) {
-            pass2_thread_v2<false>(v, acc * 1e-30f + 300.0f, 0.25f);
-#pragma unroll
-            for (int i = 0; i < kPerThread; ++i) acc += v.v[i];
-        } else if (what == 9) {
+        if (what == 7) {  // pass 1 without the warp tree
             acc += pass1_thread<V, true, false>(v, kBlockElems).m;
+            continue;
         }
-        if (what >= 7) continue;
+        if (what == 10) {  // stores through shared memory: STS, then one 64 KB bulk (TMA) store
+            float* yb = sink + (size_t)gridDim.x * kWarps + (size_t)blockIdx.x * kBlockElems;
+            float* st = reinterpret_cast<float*>(blk);
+            if (threadIdx.x == 0) bulk_wait_read<0>();
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kPerThread / 4; ++j)
+                *reinterpret_cast<float4*>(st + 4 * ((int)threadIdx.x + kThreads * j)) =
+                    make_float4(v.v[4 * j], v.v[4 * j + 1], v.v[4 * j + 2], v.v[4 * j + 3]);
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                tma_store_1d(yb, st, kBlockElems * 4, policy_evict_first());
+                bulk_commit();
+            }
+            continue;
+        }
+        if (what == 11) {  // 256-bit stores (8 consecutive floats per thread per instruction)
+            float* yb = sink + (size_t)gridDim.x * kWarps + (size_t)blockIdx.x * kBlockElems;
+#pragma unroll
+            for (int j = 0; j < kPerThread / 8; ++j) st_cs_f8(yb + 8 * ((int)threadIdx.x + kThreads * j), &v.v[8 * j]);
+            continue;
+        }
+        if (what == 8 || what == 9) {  // pass 2 with 128-bit evict-first stores to a per-CTA 64 KB buffer
+            float* yb = sink + (size_t)gridDim.x * kWarps + (size_t)blockIdx.x * kBlockElems;
+            if (what == 8) pass2_store_full<V, false>(v, acc * 1e-30f + 300.0f, 0.25f, yb);
+            else {  // stores only
+#pragma unroll
+                for (int j = 0; j < kPerThread / 4; ++j)
+                    st_cs_f4(yb + 4 * ((int)threadIdx.x + kThreads * j),
+                             make_float4(v.v[4 * j], v.v[4 * j + 1], v.v[4 * j + 2], v.v[4 * j + 3]));
+            }
+            continue;
+        }
         if (what != 1) {
             Pair wp;
             warp_pass1<V>(v, kBlockElems, &wp);
@@ -96,6 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1) bench_compute_kernel(int what, in
             for (int i = 0; i < kPerThread; ++i) acc += v.v[i];
         }
     }
+    if (threadIdx.x == 0) bulk_wait<0>();
     if ((threadIdx.x & 31) == 0) sink[blockIdx.x * kWarps + (threadIdx.x >> 5)] = acc;
 }
 

@@ -29,6 +29,11 @@ __device__ __forceinline__ void op_pass1(const BlockVals& r, int valid, Part& pa
 
 template <int V>
 __device__ __forceinline__ void op_pass2(BlockVals& r, float4 st, bool clamp, float* yb, int valid, bool vec) {
+    if (vec && valid == kBlockElems) {
+        if (clamp) pass2_store_full<V, true>(r, st.x, st.y, yb);
+        else pass2_store_full<V, false>(r, st.x, st.y, yb);
+        return;
+    }
     if (clamp) pass2_thread<true>(r, st.x, st.y);
     else pass2_thread<false>(r, st.x, st.y);
     store_block<V>(yb, valid, vec, r);

@@ -168,7 +168,7 @@ __device__ __forceinline__ float2 cl_row_stats(const float2* vals, int nb) {
     return make_float2(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m));
 }
 
-template <typename In>
+template <typename In, bool PROF>
 __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int CL, int H, int J) {
     constexpr int V = InTraits<In>::V;
     constexpr int S = ClRing<In>::S;
@@ -231,21 +231,21 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         const In* x = static_cast<const In*>(a.x);
         const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
         unsigned use_par = 0, busy = 0;  // bit s: parity of the next use of stage s / stage s in use
-        unsigned held = 0;               // 4 bits per held block of the current row: stage | parity << 3
+        unsigned held[2] = {0u, 0u};     // by row parity, 4 bits per held block: stage | parity << 3
         long long pushed = 0;
         int rr = 0;
         bool ok = true;
         unsigned long long pc_free = 0, pc_push = 0;
-        const unsigned long long pc_start = clock64();
+        const unsigned long long pc_start = PROF ? clock64() : 0ull;
 
         auto push = [&](ClCmd cmd) {
             const int c = (int)(pushed % C);
-            const unsigned long long t0 = clock64();
+            const unsigned long long t0 = PROF ? clock64() : 0ull;
             if (pushed >= C && !wait_or_abort(&cempty_bar[c], (uint32_t)(((pushed / C) - 1) & 1), err, 64u)) {
                 ok = false;
                 return;
             }
-            pc_push += clock64() - t0;
+            if (PROF) pc_push += clock64() - t0;
             cmds[c] = cmd;
             mbar_arrive(&cfull_bar[c]);
             ++pushed;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         // a free stage (its previous use fully read), round robin
         auto free_stage = [&]() -> int {
             const unsigned long long t0 = globaltimer_ns();
-            const unsigned long long c0 = clock64();
+            const unsigned long long c0 = PROF ? clock64() : 0ull;
             for (unsigned i = 0;; ++i) {
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                         busy &= ~(1u << s);
                     if (!((busy >> s) & 1u)) {
                         rr = s + 1 == S ? 0 : s + 1;
-                        pc_free += clock64() - c0;
+                        if (PROF) pc_free += clock64() - c0;
                         return s;
                     }
                 }
@@ -276,7 +276,13 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 }
             }
         };
-        auto load = [&](int s, int64_t row, int blk, uint64_t pol) -> unsigned {
+        // L2 policy per load kind (KArgs::l2_hints, env TP_L2_HINTS): 1 keep = evict_last for the
+        // pass-1 blocks pass 2 re-reads, drop = evict_first for last reads (default); 0 none;
+        // 2 keep only; 3 drop only
+        const int hints = a.l2_hints;
+        auto load = [&](int s, int64_t row, int blk, bool keep) -> unsigned {
+            const uint64_t pol = keep ? pol_keep : pol_drop;
+            const bool hinted = hints == 1 || (hints == 2 && keep) || (hints == 3 && !keep);
             const int64_t e0 = (int64_t)blk * kBlockElems;
             const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
             const unsigned parity = (use_par >> s) & 1u;
@@ -284,7 +290,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             busy |= 1u << s;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&full_bar[s], bytes);
-            tma_load_1d(stages + (size_t)s * kBlockElems, x + row * a.cols + e0, bytes, &full_bar[s], pol);
+            if (hinted) tma_load_1d(stages + (size_t)s * kBlockElems, x + row * a.cols + e0, bytes, &full_bar[s], pol);
+            else tma_load_1d_nohint(stages + (size_t)s * kBlockElems, x + row * a.cols + e0, bytes, &full_bar[s]);
             return parity;
         };
         auto p1 = [&](int k, int li0, int li1) {  // pass-1 blocks [li0, li1) of row iteration k
@@ -296,15 +303,17 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 const bool h = li >= nloc - hold;
                 const int s = free_stage();
                 if (s < 0) { ok = false; break; }
-                const unsigned par = load(s, row, b_lo + li, h ? pol_drop : pol_keep);
+                const unsigned par = load(s, row, b_lo + li, !h);
                 if (h) {
                     const int hi = li - (nloc - hold);
-                    held = (held & ~(0xfu << (4 * hi))) | ((unsigned)(s | (par << 3)) << (4 * hi));
+                    held[k & 1] = (held[k & 1] & ~(0xfu << (4 * hi))) | ((unsigned)(s | (par << 3)) << (4 * hi));
                 }
                 push(ClCmd{h ? kClP1Hold : kClP1, s, par, k, b_lo + li, 0});
             }
         };
-        auto p2 = [&](int k) {  // pass 2 of row iteration k, backwards
+        // pass 2 of row iteration k, backwards; after each pass-2 block one pass-1 block of row
+        // k + 1 from *next1 up to n1 (loads and stores of the SM interleaved)
+        auto p2 = [&](int k, int* next1, int n1) {
             int b_lo, nloc;
             cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
             const int hold = min(H, nloc);
@@ -312,13 +321,17 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             for (int li = nloc - 1; li >= 0 && ok; --li) {
                 const int fl = li == nloc - 1 ? kClFirstP2 : 0;
                 if (li >= nloc - hold) {
-                    const unsigned hs = (held >> (4 * (li - (nloc - hold)))) & 0xfu;
+                    const unsigned hs = (held[k & 1] >> (4 * (li - (nloc - hold)))) & 0xfu;
                     push(ClCmd{kClP2Held, (int)(hs & 7u), hs >> 3, k, b_lo + li, fl | (li << 8)});
                 } else {
                     const int s = free_stage();
                     if (s < 0) { ok = false; break; }
-                    const unsigned par = load(s, row, b_lo + li, pol_drop);
+                    const unsigned par = load(s, row, b_lo + li, false);
                     push(ClCmd{kClP2, s, par, k, b_lo + li, fl | (li << 8)});
+                }
+                if (*next1 < n1) {
+                    p1(k + 1, *next1, *next1 + 1);
+                    ++*next1;
                 }
             }
         };
@@ -330,17 +343,17 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
 
         if (K > 0) p1(0, 0, nloc_of(0));
         for (int k = 0; k < K && ok; ++k) {
-            int j = 0;
-            if (k + 1 < K) {  // look-ahead blocks are never held ones
-                const int n1 = nloc_of(k + 1);
+            int j = 0, n1 = 0;
+            if (k + 1 < K) {  // look-ahead blocks (never held ones) cover the row exchange
+                n1 = nloc_of(k + 1);
                 j = max(0, min(J, n1 - min(H, n1)));
                 p1(k + 1, 0, j);
             }
-            p2(k);
-            if (k + 1 < K) p1(k + 1, j, nloc_of(k + 1));
+            p2(k, &j, n1);
+            if (k + 1 < K) p1(k + 1, j, n1);
         }
         if (ok) push(ClCmd{kClExit, 0, 0, 0, 0, 0});
-        if (a.prof) {
+        if (PROF) {
             atomicAdd(&a.prof[kProfFreeStageWait], pc_free);
             atomicAdd(&a.prof[kProfPushWait], pc_push);
             atomicAdd(&a.prof[kProfProducerTotal], clock64() - pc_start);
@@ -403,16 +416,18 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     float2 st = make_float2(0.f, 0.f);
     long long np1 = 0;  // pass-1 blocks handed to the tree warp
     unsigned long long pc[kProfComputeTotal] = {0, 0, 0, 0, 0};
-    const unsigned long long pc_start = clock64();
+    const unsigned long long pc_start = PROF ? clock64() : 0ull;
     unsigned long long tq = pc_start;
     auto lap = [&](int slot) {
-        const unsigned long long t = clock64();
-        pc[slot] += t - tq;
-        tq = t;
+        if (PROF) {
+            const unsigned long long t = clock64();
+            pc[slot] += t - tq;
+            tq = t;
+        }
     };
     for (long long c = 0;; ++c) {
         const int cs = (int)(c % C);
-        tq = clock64();
+        if (PROF) tq = clock64();
         if (!wait_or_abort(&cfull_bar[cs], (uint32_t)((c / C) & 1), err, 8u)) break;
         lap(kProfCmdWait);
         const ClCmd cmd = cmds[cs];
@@ -460,7 +475,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             lap(kProfP2);
         }
     }
-    if (a.prof && warp == 0 && lane == 0) {
+    if (PROF && warp == 0 && lane == 0) {
         for (int i = 0; i < kProfComputeTotal; ++i) atomicAdd(&a.prof[i], pc[i]);
         atomicAdd(&a.prof[kProfComputeTotal], clock64() - pc_start);
     }
@@ -484,7 +499,7 @@ static int max_active_clusters(int dev, int CL, size_t dyn) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, rowcl_kernel<In>, &cfg) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveClusters(&n, rowcl_kernel<In, false>, &cfg) != cudaSuccess || n < 1) {
         cudaGetLastError();
         n = -1;
     }
@@ -501,7 +516,8 @@ template <typename In>
 static void rowcl_configure(int dev) {
     static int configured[64];
     if (!configured[dev]) {
-        cudaFuncSetAttribute(rowcl_kernel<In>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
+        cudaFuncSetAttribute(rowcl_kernel<In, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
+        cudaFuncSetAttribute(rowcl_kernel<In, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
         configured[dev] = 1;
     }
 }
@@ -570,7 +586,8 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     const int H = env_h >= 0 ? min(env_h, ClRing<In>::S - 1) : ClRing<In>::S - 1;
     const int J = env_j >= 0 ? min(env_j, kClTpSlots - 1) : 2;
     last_plan() = Plan{3, kTwoPass, ncl * CL, CL, J, H};
-    return cudaLaunchKernelEx(&cfg, rowcl_kernel<In>, a, CL, H, J);
+    if (a.prof) return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, true>, a, CL, H, J);
+    return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, H, J);
 }
 
 template int rowcl_choose<float>(int64_t, int64_t, int);

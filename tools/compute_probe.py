@@ -22,14 +22,15 @@ def main():
     ap.add_argument("--ctas", type=int, default=148)
     ap.add_argument("--reps", type=int, default=200)
     args = ap.parse_args()
-    sink = torch.empty(args.ctas * 16, dtype=torch.float32, device="cuda")
+    sink = torch.empty(args.ctas * 16 + args.ctas * 16384, dtype=torch.float32, device="cuda")
     L = tp.lib()
     st = torch.cuda.current_stream().cuda_stream
     for dt, name in ((0, "f32"), (1, "bf16")):
         ops = ((0, "pass1"), (1, "pass2"), (2, "both"))
         if dt == 0:
-            ops += ((3, "ffma2"), (4, "ffma2_imm"), (5, "ffma"), (6, "alu_addmax_shf"), (9, "pass1_thread"),
-                    (7, "pass1_thread_v2"), (8, "pass2_thread_v2"))
+            ops += ((3, "ffma2"), (4, "ffma2_imm"), (5, "ffma"), (6, "alu_addmax_shf"), (7, "pass1_thread"), (8, "pass2_with_stores"),
+                    (9, "stores_only"),
+                    (10, "stores_via_smem_tma"), (11, "stores_256bit"))
         for what, wn in ops:
             for _ in range(2):
                 assert L.tp_bench_compute(what, dt, args.ctas, args.reps, sink.data_ptr(), st) == 0
