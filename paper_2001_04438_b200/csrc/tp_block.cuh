@@ -1,9 +1,11 @@
 // Block-level pieces of the Two-Pass and Three-Pass kernels: per-thread loads (shared-memory
 // stage or global), per-thread pass computations, stores.
 //
-// A block is kBlockElems consecutive elements of one row (reading G8).  Thread t of the CTA
-// owns the vectors j = t + kThreads*k (k = 0..NV-1) of V consecutive elements (V = 4 fp32,
-// 8 bf16): every warp-wide access is a contiguous 512-byte segment.  The per-thread element
+// A block is kBlockElems consecutive elements of one row (reading G8), in two contiguous halves
+// of 8192 elements: threads 0-255 own the first half, 256-511 the second; within its half,
+// thread t owns the vectors (t mod 256) + 256 k (k = 0..NV-1) of V consecutive elements (V = 4
+// fp32, 8 bf16): every warp-wide access is a contiguous 512-byte segment, and a half block is
+// one contiguous copy (the cluster kernel stages halves separately).  The per-thread element
 // assignment, and therefore every rounding, is the same whatever the data source (TMA stage,
 // 128-bit global loads, scalar loads of misaligned rows).  A partial last block is masked
 // element by element.
@@ -11,6 +13,12 @@
 #include "tp_common.cuh"
 
 namespace tp {
+
+// Offset of vector k of thread tid in the canonical block layout (above).
+template <int V>
+__device__ __forceinline__ int vec_off(int tid, int k) {
+    return V * ((tid & 255) + 256 * k) + (tid >> 8) * (kBlockElems / 2);
+}
 
 template <typename In> struct InTraits;
 template <> struct InTraits<float> { static constexpr int V = 4; };
@@ -21,9 +29,16 @@ struct BlockVals {
     float v[kPerThread];
 };
 
+// Element offset of this thread's value i (= k*V + q).  `tid` is the thread's index in the
+// block's canonical layout: threadIdx.x, unless a kernel runs one thread's share on another
+// physical thread (tp_rowcl.cu's compute teams); the arithmetic depends only on tid.
 template <int V>
-__device__ __forceinline__ int elem_off(int i) {  // i = k*V + q
-    return V * ((int)threadIdx.x + kThreads * (i / V)) + (i % V);
+__device__ __forceinline__ int elem_off(int i, int tid) {
+    return vec_off<V>(tid, i / V) + (i % V);
+}
+template <int V>
+__device__ __forceinline__ int elem_off(int i) {
+    return elem_off<V>(i, (int)threadIdx.x);
 }
 
 __device__ __forceinline__ void unpack_bf16x8(uint4 a, float* d) {
@@ -33,11 +48,11 @@ __device__ __forceinline__ void unpack_bf16x8(uint4 a, float* d) {
 
 // From a shared-memory stage holding the block (elements past `valid` are stale: callers mask).
 template <typename In>
-__device__ __forceinline__ void load_stage(const In* stage, BlockVals& r) {
+__device__ __forceinline__ void load_stage(const In* stage, BlockVals& r, int tid = (int)threadIdx.x) {
     constexpr int V = InTraits<In>::V, NV = kPerThread / V;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        const int e = V * ((int)threadIdx.x + kThreads * k);
+        const int e = vec_off<V>(tid, k);
         if constexpr (V == 4) {
             const float4 a = *reinterpret_cast<const float4*>(stage + e);
             r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
@@ -54,7 +69,7 @@ __device__ __forceinline__ void load_global(const In* xb, int valid, bool vec, b
     constexpr int V = InTraits<In>::V, NV = kPerThread / V;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        const int e = V * ((int)threadIdx.x + kThreads * k);
+        const int e = vec_off<V>((int)threadIdx.x, k);
         if (vec && e + V <= valid) {
             if constexpr (V == 4) {
                 const float4* p = reinterpret_cast<const float4*>(xb + e);
@@ -83,7 +98,7 @@ __device__ __forceinline__ void load_global_y(const float* yb, int valid, bool v
     constexpr int NV = kPerThread / 4;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        const int e = 4 * ((int)threadIdx.x + kThreads * k);
+        const int e = vec_off<4>((int)threadIdx.x, k);
         if (vec && e + 4 <= valid) {
             const float4 a = __ldcg(reinterpret_cast<const float4*>(yb + e));
             r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
@@ -96,12 +111,13 @@ __device__ __forceinline__ void load_global_y(const float* yb, int valid, bool v
 
 // Store this thread's outputs (fp32 for every input dtype), V-element layout of In.
 template <int V>
-__device__ __forceinline__ void store_block(float* yb, int valid, bool vec, const BlockVals& r) {
+__device__ __forceinline__ void store_block(float* yb, int valid, bool vec, const BlockVals& r,
+                                            int tid = (int)threadIdx.x) {
     constexpr int NV = kPerThread / V;
     if (vec && valid == kBlockElems) {  // whole block: unconditional 128-bit stores
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
-            const int e = V * ((int)threadIdx.x + kThreads * k);
+            const int e = vec_off<V>(tid, k);
 #pragma unroll
             for (int h = 0; h < V; h += 4)
                 st_cs_f4(yb + e + h, make_float4(r.v[k * V + h], r.v[k * V + h + 1], r.v[k * V + h + 2],
@@ -111,7 +127,7 @@ __device__ __forceinline__ void store_block(float* yb, int valid, bool vec, cons
     }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        const int e = V * ((int)threadIdx.x + kThreads * k);
+        const int e = vec_off<V>(tid, k);
         if (vec && e + V <= valid) {
 #pragma unroll
             for (int h = 0; h < V; h += 4)
@@ -128,7 +144,7 @@ __device__ __forceinline__ void store_block(float* yb, int valid, bool vec, cons
 // Pass 1 on this thread's values: ExtExp and the pair accumulation
 // in 4 groups of 8 elements.  Masked elements are (m, n) = (0, -inf).
 template <int V, bool FULL, bool CLAMP>
-__device__ __forceinline__ Pair pass1_thread(const BlockVals& r, int valid) {
+__device__ __forceinline__ Pair pass1_thread(const BlockVals& r, int valid, int tid = (int)threadIdx.x) {
     AccV acc = accv_init();
 #pragma unroll
     for (int g = 0; g < kPerThread / 8; ++g) {
@@ -137,8 +153,8 @@ __device__ __forceinline__ Pair pass1_thread(const BlockVals& r, int valid) {
         for (int j = 0; j < 4; ++j) {
             ext_exp2v<CLAMP>(make_float2(r.v[8 * g + 2 * j], r.v[8 * g + 2 * j + 1]), m[j], v[j]);
             if (!FULL) {  // masked: m = 0 with v = 0 (scale 0, never the max)
-                if (!(elem_off<V>(8 * g + 2 * j) < valid)) { m[j].x = 0.0f; v[j].x = 0.0f; }
-                if (!(elem_off<V>(8 * g + 2 * j + 1) < valid)) { m[j].y = 0.0f; v[j].y = 0.0f; }
+                if (!(elem_off<V>(8 * g + 2 * j, tid) < valid)) { m[j].x = 0.0f; v[j].x = 0.0f; }
+                if (!(elem_off<V>(8 * g + 2 * j + 1, tid) < valid)) { m[j].y = 0.0f; v[j].y = 0.0f; }
             }
         }
         acc_add8v(acc, m, v);
@@ -195,7 +211,8 @@ __device__ __forceinline__ void pass2_thread(BlockVals& r, float nsum1, float la
 // Whole 16-byte aligned block: each vector's outputs stored as soon as they are computed, so
 // the stores overlap the arithmetic of the next vectors.
 template <int V, bool CLAMP>
-__device__ __forceinline__ void pass2_store_full(const BlockVals& r, float nsum1, float lam_half, float* yb) {
+__device__ __forceinline__ void pass2_store_full(const BlockVals& r, float nsum1, float lam_half, float* yb,
+                                                 int tid = (int)threadIdx.x) {
     const Pass2Consts k = pass2_consts(nsum1, lam_half);
 #pragma unroll
     for (int j = 0; j < kPerThread / V; ++j) {
@@ -206,7 +223,7 @@ __device__ __forceinline__ void pass2_store_full(const BlockVals& r, float nsum1
             o[q] = y.x;
             o[q + 1] = y.y;
         }
-        const int e = V * ((int)threadIdx.x + kThreads * j);
+        const int e = vec_off<V>(tid, j);
 #pragma unroll
         for (int h = 0; h < V; h += 4) st_cs_f4(yb + e + h, make_float4(o[h], o[h + 1], o[h + 2], o[h + 3]));
     }
@@ -286,10 +303,11 @@ __device__ __forceinline__ bool warp_pass1(const BlockVals& r, int valid, Pair* 
 // The same without the warp tree: this thread's pair (after the warp's clamp decision, which
 // *clamped receives); the tree is left to the caller (tp_rowcl.cu's tree warp).
 template <int V>
-__device__ __forceinline__ Pair thread_pass1(const BlockVals& r, int valid, bool* clamped) {
-    Pair acc = valid == kBlockElems ? pass1_thread<V, true, false>(r, valid) : pass1_thread<V, false, false>(r, valid);
+__device__ __forceinline__ Pair thread_pass1(const BlockVals& r, int valid, bool* clamped, int tid = (int)threadIdx.x) {
+    Pair acc = valid == kBlockElems ? pass1_thread<V, true, false>(r, valid, tid)
+                                    : pass1_thread<V, false, false>(r, valid, tid);
     *clamped = __any_sync(0xffffffffu, acc_out_of_domain(acc));
-    if (*clamped) acc = pass1_thread<V, false, true>(r, valid);
+    if (*clamped) acc = pass1_thread<V, false, true>(r, valid, tid);
     return acc;
 }
 

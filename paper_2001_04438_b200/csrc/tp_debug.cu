@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1) bench_compute_kernel(int what, in
             __syncthreads();
 #pragma unroll
             for (int j = 0; j < kPerThread / 4; ++j)
-                *reinterpret_cast<float4*>(st + 4 * ((int)threadIdx.x + kThreads * j)) =
+                *reinterpret_cast<float4*>(st + vec_off<4>((int)threadIdx.x, j)) =
                     make_float4(v.v[4 * j], v.v[4 * j + 1], v.v[4 * j + 2], v.v[4 * j + 3]);
             fence_proxy_async_smem();
             __syncthreads();
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1) bench_compute_kernel(int what, in
         if (what == 11) {  // 256-bit stores (8 consecutive floats per thread per instruction)
             float* yb = sink + (size_t)gridDim.x * kWarps + (size_t)blockIdx.x * kBlockElems;
 #pragma unroll
-            for (int j = 0; j < kPerThread / 8; ++j) st_cs_f8(yb + 8 * ((int)threadIdx.x + kThreads * j), &v.v[8 * j]);
+            for (int j = 0; j < kPerThread / 8; ++j) st_cs_f8(yb + vec_off<8>((int)threadIdx.x, j), &v.v[8 * j]);
             continue;
         }
         if (what == 8 || what == 9) {  // pass 2 with 128-bit evict-first stores to a per-CTA 64 KB buffer
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1) bench_compute_kernel(int what, in
             else {  // stores only
 #pragma unroll
                 for (int j = 0; j < kPerThread / 4; ++j)
-                    st_cs_f4(yb + 4 * ((int)threadIdx.x + kThreads * j),
+                    st_cs_f4(yb + vec_off<4>((int)threadIdx.x, j),
                              make_float4(v.v[4 * j], v.v[4 * j + 1], v.v[4 * j + 2], v.v[4 * j + 3]));
             }
             continue;

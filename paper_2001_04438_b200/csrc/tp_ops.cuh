@@ -28,15 +28,16 @@ __device__ __forceinline__ void op_pass1(const BlockVals& r, int valid, Part& pa
 }
 
 template <int V>
-__device__ __forceinline__ void op_pass2(BlockVals& r, float4 st, bool clamp, float* yb, int valid, bool vec) {
+__device__ __forceinline__ void op_pass2(BlockVals& r, float4 st, bool clamp, float* yb, int valid, bool vec,
+                                         int tid = (int)threadIdx.x) {
     if (vec && valid == kBlockElems) {
-        if (clamp) pass2_store_full<V, true>(r, st.x, st.y, yb);
-        else pass2_store_full<V, false>(r, st.x, st.y, yb);
+        if (clamp) pass2_store_full<V, true>(r, st.x, st.y, yb, tid);
+        else pass2_store_full<V, false>(r, st.x, st.y, yb, tid);
         return;
     }
     if (clamp) pass2_thread<true>(r, st.x, st.y);
     else pass2_thread<false>(r, st.x, st.y);
-    store_block<V>(yb, valid, vec, r);
+    store_block<V>(yb, valid, vec, r, tid);
 }
 
 // After every compute warp has run op_pass1 and a barrier among them: the row pair is the

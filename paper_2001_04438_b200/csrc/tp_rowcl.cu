@@ -34,19 +34,44 @@ namespace tp {
 
 constexpr int kClMaxNb = 256;            // blocks per row (rows of up to 4 Mi elements)
 constexpr int kClMaxLocal = 32;          // blocks per CTA per row (lane of warp 0 per block)
-constexpr int kClThreads = kThreads + 64;
+constexpr int kClThreads = kThreads + 96;  // + producer A, tree warp, producer B
 constexpr int kClCmdSlots = 16;
+constexpr int kClTeam = kWarps / 2;     // warps per compute team
 constexpr int kClTpSlots = 4;            // pass-1 thread-pair buffers between compute and tree warps
 
-template <typename In> struct ClRing { static constexpr int S = 3; };   // 3 x 64 KB fp32
-template <> struct ClRing<uint16_t> { static constexpr int S = 6; };     // 6 x 32 KB bf16
+// Half-stages: a block is staged as its two contiguous halves of 8192 elements, half h holding
+// the values of logical warps 8h..8h+7 (canonical layout, tp_block.cuh vec_off).  A compute
+// team's warp w processes logical warp w from half 0, then w + 8 from half 1, and releases each
+// half right after reading it.  192 KB: 6 x 32 KB (fp32) or 12 x 16 KB (bf16).
+template <typename In> struct ClRing {
+    static constexpr int V = InTraits<In>::V;
+    static constexpr int NV = kPerThread / V;          // vectors per thread = slices per block
+    static constexpr int kHalfElems = kBlockElems / 2;
+    static constexpr int S2 = (192 * 1024) / (kHalfElems * (int)sizeof(In));
+};
+
+// This thread's values of logical warp (8 h + wl) from half-stage `half` (see ClRing).
+template <typename In>
+__device__ __forceinline__ void load_half(const In* half, int wl, int lane, BlockVals& r) {
+    constexpr int V = InTraits<In>::V, NV = kPerThread / V;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int e = vec_off<V>(32 * wl + lane, k);  // wl < 8: offset within the half
+        if constexpr (V == 4) {
+            const float4 a = *reinterpret_cast<const float4*>(half + e);
+            r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
+        } else {
+            unpack_bf16x8(*reinterpret_cast<const uint4*>(half + e), &r.v[8 * k]);
+        }
+    }
+}
 
 enum ClOp : int { kClP1 = 0, kClP1Hold = 1, kClP2 = 2, kClP2Held = 3, kClExit = 4 };
 enum ClFlag : int { kClLastP1 = 1, kClFirstP2 = 2 };
 // development counters (KArgs::prof): clock cycles summed over CTAs
 enum ClProf : int {
     kProfCmdWait = 0, kProfFullWait, kProfRowWait, kProfP1, kProfP2, kProfComputeTotal,
-    kProfFreeStageWait, kProfPushWait, kProfProducerTotal, kProfCtas
+    kProfFreeStageWait, kProfPushWait, kProfProducerTotal, kProfCtas, kProfTeamBTotal
 };
 
 struct ClCmd {
@@ -169,13 +194,14 @@ __device__ __forceinline__ float2 cl_row_stats(const float2* vals, int nb) {
 }
 
 template <typename In, bool PROF>
-__global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int CL, int H, int J) {
+__global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int CL, int SA, int LA) {
     constexpr int V = InTraits<In>::V;
-    constexpr int S = ClRing<In>::S;
+    constexpr int S = ClRing<In>::S2;  // half-stages
+    constexpr int HE = ClRing<In>::kHalfElems;
     constexpr int C = kClCmdSlots;
     constexpr int T = kClTpSlots;
     extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ ClCmd cmds[C];
+    __shared__ ClCmd cmds[2][C];                          // team A (pass 1) / team B (pass 2) queues
     __shared__ __align__(16) Pair tpairs[T][kThreads];     // thread pairs of pass-1 blocks
     __shared__ unsigned char cbits[T][kWarps];            // per-warp clamp decisions of those blocks
     __shared__ unsigned lmask[2][kClMaxLocal];            // per-block clamp masks, by row parity
@@ -183,12 +209,13 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     __shared__ float2 row_st[2];                          // (n_sum - 1, 0.5 / m_sum) of a row
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
-    __shared__ __align__(8) uint64_t cfull_bar[C];
-    __shared__ __align__(8) uint64_t cempty_bar[C];
-    __shared__ __align__(8) uint64_t tp_full[T];           // count 16: thread pairs written
+    __shared__ __align__(8) uint64_t cfull_bar[2][C];
+    __shared__ __align__(8) uint64_t cempty_bar[2][C];
+    __shared__ __align__(8) uint64_t tp_full[T];           // count 8: thread pairs written
     __shared__ __align__(8) uint64_t tp_empty[T];          // count 1: read by the tree warp
     __shared__ __align__(8) uint64_t row_bar[2];           // count CL: one remote arrive per CTA
     __shared__ __align__(8) uint64_t st_bar[2];            // count 1: row_st written
+    __shared__ int p2_row;                                 // row iteration producer B has reached
 
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     unsigned* err = &hdr->error;
@@ -203,14 +230,15 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kWarps);
+            mbar_init(&empty_bar[s], kClTeam);
         }
-        for (int c = 0; c < C; ++c) {
-            mbar_init(&cfull_bar[c], 1);
-            mbar_init(&cempty_bar[c], kWarps);
-        }
+        for (int c = 0; c < C; ++c)
+            for (int t = 0; t < 2; ++t) {
+                mbar_init(&cfull_bar[t][c], 1);
+                mbar_init(&cempty_bar[t][c], kClTeam);
+            }
         for (int i = 0; i < T; ++i) {
-            mbar_init(&tp_full[i], kWarps);
+            mbar_init(&tp_full[i], kClTeam);
             mbar_init(&tp_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -218,22 +246,26 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             mbar_init(&st_bar[i], 1);
         }
         fence_mbar_init();
+        p2_row = -1;
     }
     __syncthreads();
     cluster_sync_all();  // every CTA's barriers are initialised before any remote arrive
 
-    if (warp == kWarps) {
-        // =============================================================== producer (lane 0)
-        // Command order: P1 of row 0; then for each row k: the first J pass-1 blocks of row k+1
-        // (work for the compute warps while the cluster exchanges row k), pass 2 of row k
-        // (held blocks first, then backwards from L2), the rest of row k+1's pass 1.
+    if (warp == kWarps || warp == kWarps + 2) {
+        // =============================================================== producers (lane 0)
+        // Producer A (warp 16) streams every pass-1 block of the CTA's rows, in order, from HBM
+        // into half-stages [0, SA) for team A; producer B (warp 18) streams the pass-2 re-reads
+        // (each row's blocks backwards, most recently loaded first: L2) into [SA, S) for team B.
+        // Separate pools: neither stream waits behind the other.  Producer A stays at most LA
+        // rows ahead of producer B, which bounds the L2 window pass 2 re-reads from.
         if (lane != 0) return;
+        const int team = warp == kWarps ? 0 : 1;
+        const int s_lo = team ? SA : 0, s_hi = team ? S : SA;
         const In* x = static_cast<const In*>(a.x);
         const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
         unsigned use_par = 0, busy = 0;  // bit s: parity of the next use of stage s / stage s in use
-        unsigned held[2] = {0u, 0u};     // by row parity, 4 bits per held block: stage | parity << 3
         long long pushed = 0;
-        int rr = 0;
+        int rr = s_lo;
         bool ok = true;
         unsigned long long pc_free = 0, pc_push = 0;
         const unsigned long long pc_start = PROF ? clock64() : 0ull;
@@ -241,28 +273,27 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         auto push = [&](ClCmd cmd) {
             const int c = (int)(pushed % C);
             const unsigned long long t0 = PROF ? clock64() : 0ull;
-            if (pushed >= C && !wait_or_abort(&cempty_bar[c], (uint32_t)(((pushed / C) - 1) & 1), err, 64u)) {
+            if (pushed >= C && !wait_or_abort(&cempty_bar[team][c], (uint32_t)(((pushed / C) - 1) & 1), err, 64u)) {
                 ok = false;
                 return;
             }
             if (PROF) pc_push += clock64() - t0;
-            cmds[c] = cmd;
-            mbar_arrive(&cfull_bar[c]);
+            cmds[team][c] = cmd;
+            mbar_arrive(&cfull_bar[team][c]);
             ++pushed;
         };
-        // a free stage (its previous use fully read), round robin
+        // a free half-stage of this pool (its previous use fully read), round robin
         auto free_stage = [&]() -> int {
             const unsigned long long t0 = globaltimer_ns();
             const unsigned long long c0 = PROF ? clock64() : 0ull;
             for (unsigned i = 0;; ++i) {
-#pragma unroll
-                for (int j = 0; j < S; ++j) {
+                for (int j = 0; j < s_hi - s_lo; ++j) {
                     int s = rr + j;
-                    s = s >= S ? s - S : s;
+                    s = s >= s_hi ? s - (s_hi - s_lo) : s;
                     if (((busy >> s) & 1u) && mbar_test_parity(&empty_bar[s], ((use_par >> s) & 1u) ^ 1u))
                         busy &= ~(1u << s);
                     if (!((busy >> s) & 1u)) {
-                        rr = s + 1 == S ? 0 : s + 1;
+                        rr = s + 1 == s_hi ? s_lo : s + 1;
                         if (PROF) pc_free += clock64() - c0;
                         return s;
                     }
@@ -277,83 +308,70 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             }
         };
         // L2 policy per load kind (KArgs::l2_hints, env TP_L2_HINTS): 1 keep = evict_last for the
-        // pass-1 blocks pass 2 re-reads, drop = evict_first for last reads (default); 0 none;
+        // pass-1 loads pass 2 re-reads, drop = evict_first for the re-reads (default); 0 none;
         // 2 keep only; 3 drop only
         const int hints = a.l2_hints;
-        auto load = [&](int s, int64_t row, int blk, bool keep) -> unsigned {
+        // half h of a block into half-stage s: one bulk copy, clipped to the row's valid elements
+        auto load_h = [&](int s, int64_t row, int blk, int h, bool keep) -> unsigned {
             const uint64_t pol = keep ? pol_keep : pol_drop;
             const bool hinted = hints == 1 || (hints == 2 && keep) || (hints == 3 && !keep);
-            const int64_t e0 = (int64_t)blk * kBlockElems;
-            const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
+            const int64_t e0 = (int64_t)blk * kBlockElems + (int64_t)h * HE;
+            const int n = (int)max((int64_t)0, min((int64_t)HE, a.cols - e0));
+            const uint32_t bytes = (uint32_t)n * (uint32_t)sizeof(In);
             const unsigned parity = (use_par >> s) & 1u;
             use_par ^= 1u << s;
             busy |= 1u << s;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&full_bar[s], bytes);
-            if (hinted) tma_load_1d(stages + (size_t)s * kBlockElems, x + row * a.cols + e0, bytes, &full_bar[s], pol);
-            else tma_load_1d_nohint(stages + (size_t)s * kBlockElems, x + row * a.cols + e0, bytes, &full_bar[s]);
+            if (n > 0) {
+                In* dst = stages + (size_t)s * HE;
+                const In* src = x + row * a.cols + e0;
+                if (hinted) tma_load_1d(dst, src, bytes, &full_bar[s], pol);
+                else tma_load_1d_nohint(dst, src, bytes, &full_bar[s]);
+            }
             return parity;
         };
-        auto p1 = [&](int k, int li0, int li1) {  // pass-1 blocks [li0, li1) of row iteration k
-            int b_lo, nloc;
-            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
-            const int hold = min(H, nloc);
-            const int64_t row = cid + (int64_t)k * ncl;
-            for (int li = li0; li < li1 && ok; ++li) {
-                const bool h = li >= nloc - hold;
-                const int s = free_stage();
-                if (s < 0) { ok = false; break; }
-                const unsigned par = load(s, row, b_lo + li, !h);
-                if (h) {
-                    const int hi = li - (nloc - hold);
-                    held[k & 1] = (held[k & 1] & ~(0xfu << (4 * hi))) | ((unsigned)(s | (par << 3)) << (4 * hi));
-                }
-                push(ClCmd{h ? kClP1Hold : kClP1, s, par, k, b_lo + li, 0});
-            }
-        };
-        // pass 2 of row iteration k, backwards; after each pass-2 block one pass-1 block of row
-        // k + 1 from *next1 up to n1 (loads and stores of the SM interleaved)
-        auto p2 = [&](int k, int* next1, int n1) {
-            int b_lo, nloc;
-            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
-            const int hold = min(H, nloc);
-            const int64_t row = cid + (int64_t)k * ncl;
-            for (int li = nloc - 1; li >= 0 && ok; --li) {
-                const int fl = li == nloc - 1 ? kClFirstP2 : 0;
-                if (li >= nloc - hold) {
-                    const unsigned hs = (held[k & 1] >> (4 * (li - (nloc - hold)))) & 0xfu;
-                    push(ClCmd{kClP2Held, (int)(hs & 7u), hs >> 3, k, b_lo + li, fl | (li << 8)});
-                } else {
-                    const int s = free_stage();
-                    if (s < 0) { ok = false; break; }
-                    const unsigned par = load(s, row, b_lo + li, false);
-                    push(ClCmd{kClP2, s, par, k, b_lo + li, fl | (li << 8)});
-                }
-                if (*next1 < n1) {
-                    p1(k + 1, *next1, *next1 + 1);
-                    ++*next1;
-                }
-            }
-        };
-        auto nloc_of = [&](int k) {
-            int b_lo, nloc;
-            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
-            return nloc;
+        // both halves of a block: returns (s0 | par0 << 4 | s1 << 5 | par1 << 9), or -1
+        auto load = [&](int64_t row, int blk, bool keep) -> int {
+            const int s0 = free_stage();
+            if (s0 < 0) return -1;
+            const unsigned p0 = load_h(s0, row, blk, 0, keep);
+            const int s1 = free_stage();
+            if (s1 < 0) return -1;
+            const unsigned p1 = load_h(s1, row, blk, 1, keep);
+            return (int)((unsigned)s0 | (p0 << 4) | ((unsigned)s1 << 5) | (p1 << 9));
         };
 
-        if (K > 0) p1(0, 0, nloc_of(0));
         for (int k = 0; k < K && ok; ++k) {
-            int j = 0, n1 = 0;
-            if (k + 1 < K) {  // look-ahead blocks (never held ones) cover the row exchange
-                n1 = nloc_of(k + 1);
-                j = max(0, min(J, n1 - min(H, n1)));
-                p1(k + 1, 0, j);
+            int b_lo, nloc;
+            cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
+            const int64_t row = cid + (int64_t)k * ncl;
+            if (team == 0) {
+                // lead limit: row k's pass-1 loads wait until producer B has started row k - LA
+                const unsigned long long t0 = globaltimer_ns();
+                for (unsigned i = 0; *reinterpret_cast<volatile int*>(&p2_row) < k - LA; ++i) {
+                    if ((i & 63u) == 63u && (aborted(err) || globaltimer_ns() - t0 > kWaitTimeoutNs)) {
+                        atomicOr(err, 2048u);
+                        ok = false;
+                        break;
+                    }
+                }
+                for (int li = 0; li < nloc && ok; ++li) {
+                    const int st = load(row, b_lo + li, true);
+                    if (st < 0) { ok = false; break; }
+                    push(ClCmd{kClP1, st, 0u, k, b_lo + li, 0});
+                }
+            } else {
+                *reinterpret_cast<volatile int*>(&p2_row) = k;
+                for (int li = nloc - 1; li >= 0 && ok; --li) {
+                    const int st = load(row, b_lo + li, false);
+                    if (st < 0) { ok = false; break; }
+                    push(ClCmd{kClP2, st, 0u, k, b_lo + li, (li == nloc - 1 ? kClFirstP2 : 0) | (li << 8)});
+                }
             }
-            p2(k, &j, n1);
-            if (k + 1 < K) p1(k + 1, j, n1);
         }
         if (ok) push(ClCmd{kClExit, 0, 0, 0, 0, 0});
-        if (PROF) {
+        if (PROF && team == 0) {
             atomicAdd(&a.prof[kProfFreeStageWait], pc_free);
             atomicAdd(&a.prof[kProfPushWait], pc_push);
             atomicAdd(&a.prof[kProfProducerTotal], clock64() - pc_start);
@@ -361,7 +379,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         }
         return;
     }
-    if (warp > kWarps) {
+    if (warp == kWarps + 1) {
         // =============================================================== tree warp
         // Per pass-1 block, in command order: the perfect tree over the 512 thread pairs in
         // thread order (lane l reduces threads 16l..16l+15, then the warp tree) = the stream
@@ -412,9 +430,16 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         return;
     }
 
-    // =================================================================== compute warps
+    // =================================================================== compute teams
+    // Team A (warps 0-7) runs every pass-1 command, team B (warps 8-15) every pass-2 command, so
+    // an SM's loads, arithmetic and output stores stay interleaved (one SM's store path moves
+    // ~32 B/clock: a lone pass-2 phase would stall on it).  Physical warp w of a team computes
+    // the block's logical warps w and w + 8 in turn: thread tid = 32 * logical warp + lane of
+    // the canonical layout, so every rounding is that of the 16-warp kernels.
+    const bool teamB = warp >= kClTeam;
+    const int pw = teamB ? warp - kClTeam : warp;
     float2 st = make_float2(0.f, 0.f);
-    long long np1 = 0;  // pass-1 blocks handed to the tree warp
+    long long np1 = 0;  // pass-1 blocks handed to the tree warp (team A)
     unsigned long long pc[kProfComputeTotal] = {0, 0, 0, 0, 0};
     const unsigned long long pc_start = PROF ? clock64() : 0ull;
     unsigned long long tq = pc_start;
@@ -428,56 +453,71 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     for (long long c = 0;; ++c) {
         const int cs = (int)(c % C);
         if (PROF) tq = clock64();
-        if (!wait_or_abort(&cfull_bar[cs], (uint32_t)((c / C) & 1), err, 8u)) break;
+        if (!wait_or_abort(&cfull_bar[teamB][cs], (uint32_t)((c / C) & 1), err, 8u)) break;
         lap(kProfCmdWait);
-        const ClCmd cmd = cmds[cs];
+        const ClCmd cmd = cmds[teamB][cs];
         __syncwarp();
-        if (lane == 0) mbar_arrive(&cempty_bar[cs]);
+        if (lane == 0) mbar_arrive(&cempty_bar[teamB][cs]);
         if (cmd.op == kClExit) break;
         const int64_t row = cid + (int64_t)cmd.k * ncl;
         const int blk = cmd.li;  // absolute block index
         const int valid = (int)min((int64_t)kBlockElems, a.cols - (int64_t)blk * kBlockElems);
         const int par = cmd.k & 1;
-        In* stage = stages + (size_t)cmd.stage * kBlockElems;
+        // the block's two half-stages and their full-barrier parities (ClCmd::stage packing)
+        const int st_pack = cmd.stage;
         BlockVals v;
-        if (cmd.op == kClP1 || cmd.op == kClP1Hold) {
-            if (!wait_or_abort(&full_bar[cmd.stage], cmd.parity, err, 4u)) break;
-            lap(kProfFullWait);
-            load_stage<In>(stage, v);
-            if (cmd.op == kClP1) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[cmd.stage]);
-            }
-            bool cl;
-            const Pair tp_ = thread_pass1<V>(v, valid, &cl);
+        bool fail = false;
+        if (!teamB) {
             const int sl = (int)(np1 % T);
             if (np1 >= T && !wait_or_abort(&tp_empty[sl], (uint32_t)(((np1 / T) - 1) & 1), err, 1024u)) break;
             ++np1;
-            tpairs[sl][threadIdx.x] = tp_;
-            if (lane == 0) cbits[sl][warp] = cl ? 1 : 0;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int lw = pw + kClTeam * h, tid = 32 * lw + lane;
+                const int sh = (st_pack >> (5 * h)) & 15;
+                const uint32_t ph = (uint32_t)(st_pack >> (5 * h + 4)) & 1u;
+                if (!wait_or_abort(&full_bar[sh], ph, err, 4u)) { fail = true; break; }
+                lap(kProfFullWait);
+                load_half<In>(stages + (size_t)sh * HE, pw, lane, v);
+                if (cmd.op == kClP1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[sh]);
+                }
+                bool cl;
+                tpairs[sl][tid] = thread_pass1<V>(v, valid, &cl, tid);
+                if (lane == 0) cbits[sl][lw] = cl ? 1 : 0;
+                lap(kProfP1);
+            }
+            if (fail) break;
             __syncwarp();
             if (lane == 0) mbar_arrive(&tp_full[sl]);
-            lap(kProfP1);
         } else {
             if (cmd.flags & kClFirstP2) {  // the row's statistics, from the tree warp
                 if (!wait_or_abort(&st_bar[par], (uint32_t)((cmd.k >> 1) & 1), err, 256u)) break;
                 st = row_st[par];
                 lap(kProfRowWait);
             }
-            if (cmd.op == kClP2 && !wait_or_abort(&full_bar[cmd.stage], cmd.parity, err, 4u)) break;
-            lap(kProfFullWait);
-            load_stage<In>(stage, v);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[cmd.stage]);
-            const bool my_clamp = ((lmask[par][cmd.flags >> 8] >> warp) & 1u) != 0;
-            op_pass2<V>(v, make_float4(st.x, st.y, 0.f, 0.f), my_clamp, a.y + row * a.cols + (int64_t)blk * kBlockElems,
-                        valid, true);
-            lap(kProfP2);
+            const unsigned mask = lmask[par][cmd.flags >> 8];
+            float* yb = a.y + row * a.cols + (int64_t)blk * kBlockElems;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int lw = pw + kClTeam * h, tid = 32 * lw + lane;
+                const int sh = (st_pack >> (5 * h)) & 15;
+                const uint32_t ph = (uint32_t)(st_pack >> (5 * h + 4)) & 1u;
+                if (cmd.op == kClP2 && !wait_or_abort(&full_bar[sh], ph, err, 4u)) { fail = true; break; }
+                lap(kProfFullWait);
+                load_half<In>(stages + (size_t)sh * HE, pw, lane, v);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[sh]);
+                op_pass2<V>(v, make_float4(st.x, st.y, 0.f, 0.f), ((mask >> lw) & 1u) != 0, yb, valid, true, tid);
+                lap(kProfP2);
+            }
+            if (fail) break;
         }
     }
-    if (PROF && warp == 0 && lane == 0) {
+    if (PROF && pw == 0 && lane == 0) {
         for (int i = 0; i < kProfComputeTotal; ++i) atomicAdd(&a.prof[i], pc[i]);
-        atomicAdd(&a.prof[kProfComputeTotal], clock64() - pc_start);
+        atomicAdd(&a.prof[teamB ? kProfTeamBTotal : kProfComputeTotal], clock64() - pc_start);
     }
 }
 
@@ -509,7 +549,7 @@ static int max_active_clusters(int dev, int CL, size_t dyn) {
 
 template <typename In>
 static size_t rowcl_dyn_smem() {
-    return (size_t)ClRing<In>::S * kBlockElems * sizeof(In);
+    return (size_t)ClRing<In>::S2 * ClRing<In>::kHalfElems * sizeof(In);
 }
 
 template <typename In>
@@ -533,7 +573,7 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl) {
     rowcl_configure<In>(dev);
     const size_t dyn = rowcl_dyn_smem<In>();
     const double block_bytes = (double)kBlockElems * sizeof(In);
-    const int H = ClRing<In>::S - 1;
+    const int H = 0;  // no block stays staged between the passes
     int best = 0;
     double best_t = 0.0;
     for (int CL = 1; CL <= 8; CL *= 2) {
@@ -575,19 +615,22 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static const int env_h = [] {
-        const char* e = getenv("TP_CL_HOLD");
+    // development overrides: TP_CL_POOL_A = half-stages of the pass-1 pool, TP_CL_LEAD = rows
+    // producer A may run ahead of producer B
+    static const int env_sa = [] {
+        const char* e = getenv("TP_CL_POOL_A");
         return e ? atoi(e) : -1;
     }();
-    static const int env_j = [] {
-        const char* e = getenv("TP_CL_LOOKAHEAD");
+    static const int env_la = [] {
+        const char* e = getenv("TP_CL_LEAD");
         return e ? atoi(e) : -1;
     }();
-    const int H = env_h >= 0 ? min(env_h, ClRing<In>::S - 1) : ClRing<In>::S - 1;
-    const int J = env_j >= 0 ? min(env_j, kClTpSlots - 1) : 2;
-    last_plan() = Plan{3, kTwoPass, ncl * CL, CL, J, H};
-    if (a.prof) return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, true>, a, CL, H, J);
-    return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, H, J);
+    constexpr int S2 = ClRing<In>::S2;
+    const int SA = env_sa >= 2 && env_sa <= S2 - 2 ? env_sa : S2 / 2;
+    const int LA = env_la >= 1 ? env_la : 1;
+    last_plan() = Plan{3, kTwoPass, ncl * CL, CL, LA, SA};
+    if (a.prof) return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, true>, a, CL, SA, LA);
+    return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, SA, LA);
 }
 
 template int rowcl_choose<float>(int64_t, int64_t, int);

@@ -17,8 +17,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2001_04438_b200 as tp  # noqa: E402
 import workloads  # noqa: E402
 
-SLOTS = ["cmd_wait", "full_wait", "row_wait_and_stats", "p1_compute", "p2_compute", "compute_total",
-         "prod_free_stage_wait", "prod_push_wait", "prod_total", "ctas"]
+SLOTS = ["cmd_wait", "full_wait", "row_wait_and_stats", "p1_compute", "p2_compute", "teamA_total",
+         "prod_free_stage_wait", "prod_push_wait", "prod_total", "ctas", "teamB_total"]
 
 
 def main():
@@ -43,11 +43,11 @@ def main():
     tp.lib().tp_set_profile_buffer(None)
     c = buf.cpu().numpy().astype(np.float64)
     ctas = c[9]
-    per = {SLOTS[i]: c[i] / ctas for i in range(9)}
-    tot = per["compute_total"]
+    per = {SLOTS[i]: c[i] / ctas for i in range(11) if i != 9}
+    tot = per["teamA_total"] + per["teamB_total"]
     out = {"config": args.config, "plan": tp.last_plan(), "us_per_launch": s.elapsed_time(e) * 1e3 / args.reps,
            "cycles_per_cta": {k: round(v) for k, v in per.items()},
-           "compute_share": {k: round(per[k] / tot, 3) for k in SLOTS[:5]},
+           "share_of_both_teams": {k: round(per[k] / tot, 3) for k in SLOTS[:5]},
            "producer_share": {k: round(per[k] / per["prod_total"], 3) for k in SLOTS[6:8]}}
     print(json.dumps(out), flush=True)
 
