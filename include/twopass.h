@@ -185,6 +185,12 @@ int tp_debug_op(int what, const float* a, const float* b, float* out0, float* ou
  * (tools/prof_roles.py documents the slots); NULL switches it off. */
 int tp_set_profile_buffer(void* device_counters);
 
+/* STREAM-style HBM baselines beside the softmax passes (measurement only):
+ * what = 0 copy y = x (8 B/element), 1 scale y = a x (8), 2 in-place scale x = a x (8),
+ * 3 read-only sum (4 B/element; one partial per CTA written to y[0..ctas)).  Device pointers,
+ * 16-byte aligned, n a multiple of 4; ctas = grid size (0 = 4 per SM).  Asynchronous. */
+int tp_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t stream);
+
 int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink, cudaStream_t stream);
 
 #ifdef __cplusplus

@@ -420,6 +420,21 @@ int tp_set_profile_buffer(void* p) {
     return TP_OK;
 }
 
+int tp_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t stream) {
+    if (what < 0 || what > 3 || n < 0 || (n & 3) || !x || (what != 2 && !y) ||
+        ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15))
+        return TP_EINVAL;
+    if (n == 0) return TP_OK;
+    if (ctas <= 0) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        ctas = 4 * (int64_t)sms;
+    }
+    cudaError_t e = tp::launch_stream_baseline(what, x, y, n, a, ctas, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
 int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink, cudaStream_t stream) {
     if (what < 0 || what > 11 || ctas < 1 || reps < 1 || !sink || (in_dtype != TP_IN_F32 && in_dtype != TP_IN_BF16))
         return TP_EINVAL;

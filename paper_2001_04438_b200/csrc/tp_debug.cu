@@ -140,6 +140,49 @@ cudaError_t launch_bench_compute(int what, int in_bf16, int64_t ctas, int reps, 
     return cudaGetLastError();
 }
 
+// STREAM-style bandwidth baselines (measurement only, not part of the method):
+// 0 copy y = x, 1 scale y = a x, 2 in-place scale x = a x, 3 read-only sum (one partial per
+// CTA into y).  128-bit accesses, grid-stride, n a multiple of 4 and 16-byte aligned pointers.
+__global__ void __launch_bounds__(512) stream_baseline_kernel(int what, float* x, float* y, int64_t n4, float a) {
+    float4* x4 = reinterpret_cast<float4*>(x);
+    float4* y4 = reinterpret_cast<float4*>(y);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float s = 0.0f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += 4 * stride) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i + u * stride < n4) v[u] = __ldcs(x4 + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i + u * stride >= n4) continue;
+            if (what == 3) {
+                s += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+                continue;
+            }
+            if (what != 0) v[u] = make_float4(a * v[u].x, a * v[u].y, a * v[u].z, a * v[u].w);
+            __stcs((what == 2 ? x4 : y4) + i + u * stride, v[u]);
+        }
+    }
+    if (what == 3) {
+        __shared__ float red[16];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float t = 0.0f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            y[blockIdx.x] = t;
+        }
+    }
+}
+
+cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t s) {
+    stream_baseline_kernel<<<(unsigned)ctas, 512, 0, s>>>(what, x, y, n / 4, a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_debug(int what, const float* a, const float* b, float* o0, float* o1, int64_t count,
                          cudaStream_t s) {
     if (count <= 0) return cudaSuccess;
