@@ -191,6 +191,19 @@ int tp_set_profile_buffer(void* device_counters);
  * 16-byte aligned, n a multiple of 4; ctas = grid size (0 = 4 per SM).  Asynchronous. */
 int tp_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t stream);
 
+/* Accuracy sweep hook (test/metrology only): for i < count, x = the fp32 whose
+ * bit pattern is bits0 + i (the caller keeps bits0 + count - 1 <= 0xffffffff); what = 0:
+ * ExtExp -> out0 = m, out1 = n; what = 1: Exp with reconstruction (Alg. 4,
+ * PAPER.md:234-249) -> out0.  Device output arrays of count floats. */
+int tp_exp_sweep(int what, uint32_t bits0, int64_t count, float* out0, float* out1, cudaStream_t stream);
+
+/* Coefficient-search hook (tools/fit_exp_gpu.py; not part of the method): grades Alg. 4's Exp
+ * with the HOST coefficients coeffs[0..4] = c1..c5 against the double exponential on
+ * x = as_float(bits0 + i * stride), i < count (normal outputs): *max_ulp_bits (device uint,
+ * atomicMax of the float bits; zero it first) and *n_over2 (device uint64, count above 2 ulp). */
+int tp_exp_fit(const float* coeffs, uint32_t bits0, int64_t count, int stride, unsigned* max_ulp_bits,
+               unsigned long long* n_over2, cudaStream_t stream);
+
 int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink, cudaStream_t stream);
 
 #ifdef __cplusplus

@@ -34,7 +34,7 @@ EXPORTS = [
     "softmax_bf16_partial", "softmax_f32_finish", "softmax_bf16_f32_finish", "softmax_workspace_bytes",
     "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_f32_host", "softmax_bf16_f32_host",
     "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
-    "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline",
+    "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_exp_sweep", "tp_exp_fit",
 ]
 
 
@@ -86,6 +86,8 @@ def lib() -> ctypes.CDLL:
         L.tp_debug_op.argtypes = [ci, vp, vp, vp, vp, i64, vp]
         L.softmax_watchdog_flags.argtypes = [vp, ci]
         L.tp_set_profile_buffer.argtypes = [vp]
+        L.tp_exp_fit.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_uint32, i64, ci, vp, vp, vp]
+        L.tp_exp_sweep.argtypes = [ci, ctypes.c_uint32, i64, vp, vp, vp]
         L.tp_stream_baseline.argtypes = [ci, vp, vp, i64, ctypes.c_float, i64, vp]
         L.tp_bench_compute.argtypes = [ci, ci, i64, ci, vp, vp]
         L.softmax_last_plan.argtypes = [ctypes.POINTER(SoftmaxPlan)]

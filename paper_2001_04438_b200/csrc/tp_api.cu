@@ -435,6 +435,23 @@ int tp_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 
+int tp_exp_sweep(int what, uint32_t bits0, int64_t count, float* out0, float* out1, cudaStream_t stream) {
+    if (what < 0 || what > 1 || count < 0 || (count > 0 && (!out0 || (what == 0 && !out1))) ||
+        (uint64_t)bits0 + (uint64_t)count > 0x100000000ull)
+        return TP_EINVAL;
+    cudaError_t e = tp::launch_exp_sweep(what, bits0, count, out0, out1, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int tp_exp_fit(const float* coeffs, uint32_t bits0, int64_t count, int stride, unsigned* max_ulp_bits,
+               unsigned long long* n_over2, cudaStream_t stream) {
+    if (!coeffs || count < 0 || stride < 1 || (count > 0 && (!max_ulp_bits || !n_over2)) ||
+        (uint64_t)bits0 + (uint64_t)count * (uint64_t)stride > 0x100000000ull)
+        return TP_EINVAL;
+    cudaError_t e = tp::launch_exp_fit(coeffs, bits0, count, stride, max_ulp_bits, n_over2, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
 int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink, cudaStream_t stream) {
     if (what < 0 || what > 11 || ctas < 1 || reps < 1 || !sink || (in_dtype != TP_IN_F32 && in_dtype != TP_IN_BF16))
         return TP_EINVAL;

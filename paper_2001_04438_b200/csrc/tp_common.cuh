@@ -28,14 +28,16 @@ constexpr float kMagic = 0x1.8p23f;
 constexpr float kXClamp = 0x1.0p21f;
 constexpr float kNLimit = 3025525.5f;             // > round(2^21 log2 e) = 3025525
 // Degree-5 polynomial p(t) = 1 + t(c1 + t(c2 + t(c3 + t(c4 + t c5)))) for e^t on
-// |t| <= 0.3476.  The paper's Sollya coefficients are not printed
-// (reading G3); these come from tools/fit_exp_poly.py (relative minimax + fp32
-// neighbourhood search, max 1.96 ulp for the fp32 Horner evaluation).
-constexpr float kC1 = 0x1.fffff6p-1f;   // 0.999999702
-constexpr float kC2 = 0x1.fffddap-2f;   // 0.499991804
-constexpr float kC3 = 0x1.555a30p-3f;   // 0.166675925
-constexpr float kC4 = 0x1.5738e8p-5f;   // 0.0418972522
-constexpr float kC5 = 0x1.1000a8p-7f;   // 0.00830085948
+// |t| <= ln2/2.  The paper's Sollya coefficients are not printed (reading G3);
+// these come from tools/fit_exp_gpu.py: minimax in fp32-ulp units (linear program), rounded to
+// binary32, then coordinate / pairwise binary32 searches graded on the GPU end to end.  Alg. 4's
+// Exp is then within 1.90 ulp of e^x on every fp32 x in [ln FLT_MIN, 0] (exhaustive,
+// tools/exp_accuracy.py; the paper's "under 2 ULP").
+constexpr float kC1 = 0x1.ffffeep-1f;   // 0.99999946
+constexpr float kC2 = 0x1.fffdc6p-2f;   // 0.4999915
+constexpr float kC3 = 0x1.555d92p-3f;   // 0.16668238
+constexpr float kC4 = 0x1.573998p-5f;   // 0.04189758
+constexpr float kC5 = 0x1.0e8b38p-7f;   // 0.008256342
 
 // Canonical decomposition of a row (reading G8): blocks of kBlockElems elements,
 // groups of kGroupBlocks blocks.  These, not the grid size, fix every rounding.

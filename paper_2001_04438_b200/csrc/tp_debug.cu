@@ -183,6 +183,70 @@ cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, floa
     return cudaGetLastError();
 }
 
+// Exhaustive accuracy sweeps: x = the fp32 with bit pattern bits0 + i.
+// what 0: ExtExp -> (m, n); 1: Exp with reconstruction (Alg. 4) -> y.
+__global__ void exp_sweep_kernel(int what, uint32_t bits0, int64_t count, float* o0, float* o1) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const float x = __uint_as_float(bits0 + (uint32_t)i);
+    if (what == 0) {
+        const Pair p = ext_exp(x);
+        o0[i] = p.m;
+        o1[i] = p.n;
+    } else {
+        o0[i] = exp_flush2(make_float2(x, x)).x;
+    }
+}
+
+cudaError_t launch_exp_sweep(int what, uint32_t bits0, int64_t count, float* o0, float* o1, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    exp_sweep_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(what, bits0, count, o0, o1);
+    return cudaGetLastError();
+}
+
+// Coefficient search support (tools/fit_exp_gpu.py): the Exp of Alg. 4 with runtime
+// coefficients c[0..4] = c1..c5 (same fp32 operations as exp_flush2), graded against the double
+// exponential: max ulp (as float bits, atomicMax) and the count above 2 ulp over the inputs
+// x = as_float(bits0 + i * stride), i < count.  Normal outputs only (x >= ln FLT_MIN).
+__global__ void exp_fit_kernel(float c1, float c2, float c3, float c4, float c5, uint32_t bits0, int64_t count,
+                               int stride, unsigned* max_bits, unsigned long long* n_over2) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float err = 0.0f;
+    if (i < count) {
+        const float x = __uint_as_float(bits0 + (uint32_t)(i * stride));
+        const float v = __fmaf_rn(x, kLog2e, kMagic);
+        const float n = __fsub_rn(v, kMagic);
+        float t = __fmaf_rn(n, -kLn2Hi, x);
+        t = __fmaf_rn(n, -kLn2Lo, t);
+        float p = __fmaf_rn(c5, t, c4);
+        p = __fmaf_rn(p, t, c3);
+        p = __fmaf_rn(p, t, c2);
+        p = __fmaf_rn(p, t, c1);
+        p = __fmaf_rn(p, t, 1.0f);
+        const float y = __fmul_rn(p, pow2_bits(__float_as_int(v) - (magic_bits() - 127)));
+        const double ref = exp((double)x);
+        int e;
+        frexp(ref, &e);  // ref = f 2^e, f in [0.5, 1): fp32 ulp = 2^(e - 24)
+        err = (float)(fabs((double)y - ref) / ldexp(1.0, e - 24));
+    }
+    unsigned long long over = __ballot_sync(0xffffffffu, err > 2.0f);
+    float m = err;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(max_bits, __float_as_uint(m));
+        if (over) atomicAdd(n_over2, (unsigned long long)__popc((unsigned)over));
+    }
+}
+
+cudaError_t launch_exp_fit(const float* c, uint32_t bits0, int64_t count, int stride, unsigned* max_bits,
+                           unsigned long long* n_over2, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    exp_fit_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(c[0], c[1], c[2], c[3], c[4], bits0, count, stride,
+                                                                   max_bits, n_over2);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_debug(int what, const float* a, const float* b, float* o0, float* o1, int64_t count,
                          cudaStream_t s) {
     if (count <= 0) return cudaSuccess;

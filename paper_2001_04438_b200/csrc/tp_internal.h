@@ -61,6 +61,9 @@ cudaError_t launch_finish(int in_bf16, const void* x, float* y, int64_t rows, in
 cudaError_t launch_debug(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                          cudaStream_t s);
 cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t s);
+cudaError_t launch_exp_sweep(int what, uint32_t bits0, int64_t count, float* o0, float* o1, cudaStream_t s);
+cudaError_t launch_exp_fit(const float* c, uint32_t bits0, int64_t count, int stride, unsigned* max_bits,
+                           unsigned long long* n_over2, cudaStream_t s);
 cudaError_t launch_bench_compute(int what, int in_bf16, int64_t ctas, int reps, float* sink, cudaStream_t s);
 
 }  // namespace tp

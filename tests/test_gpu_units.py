@@ -144,3 +144,42 @@ def test_exp_with_reconstruction_ulp():
     assert err.max() <= 3.0, err.max()
     assert np.all(e[~normal] <= np.float32(np.finfo(np.float32).tiny))
     assert e[-1] == 0.0 and e[-2] == 0.0
+
+
+# ------------------------------------------------------------------ exhaustive-lite ULP metrology (NEXT-2)
+
+def _ulp32(v):
+    v = np.asarray(v, np.float64)
+    return np.exp2(np.floor(np.log2(v)) - 23)
+
+
+@pytest.mark.parametrize("what", ["exp", "extexp"])
+def test_exp_within_2_ulp_on_strided_fp32_sweep(what):
+    # "maximum error under 2 ULP, validated through exhaustive evaluation".  The
+    # exhaustive run is tools/exp_accuracy.py (profiles/r01b_exp_accuracy.json: 1.95 / 1.96 ulp);
+    # here every 1021st fp32 of the domain, graded against the oracle's long-double definitions.
+    import struct
+    L = tp.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    f2b = lambda v: struct.unpack("<I", struct.pack("<f", v))[0]  # noqa: E731
+    if what == "exp":   # Alg. 4 on x in [ln FLT_MIN, 0] (normal outputs)
+        spans = [(f2b(-0.0), f2b(-87.33654))]
+    else:               # ExtExp on |x| <= 1e4 (the configurations' domain)
+        spans = [(f2b(0.0), f2b(1e4)), (f2b(-0.0), f2b(-1e4))]
+    worst = 0.0
+    for b0, b1 in spans:
+        bits = np.arange(b0, b1 + 1, 1021, dtype=np.uint64).astype(np.uint32)
+        x = bits.view(np.float32)
+        xd = torch.from_numpy(x.copy()).cuda()
+        if what == "exp":
+            y = tp.debug_op(3, xd)
+            y = (y[0] if isinstance(y, tuple) else y).cpu().numpy()
+            ref = oracle.exp_scaled(x, np.zeros(x.size))          # e^x in long double
+            got = y
+        else:
+            m, n = tp.debug_op(0, xd)
+            got, n = m.cpu().numpy(), n.cpu().numpy()
+            ref = oracle.exp_scaled(x, n.astype(np.float64))      # e^x 2^-n: the m the pair must carry
+        err = np.abs(got.astype(np.longdouble) - ref).astype(np.float64) / _ulp32(ref.astype(np.float64))
+        worst = max(worst, float(err.max()))
+    assert worst < 2.0, worst
