@@ -199,7 +199,7 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
     if (a.vec && !o.no_tma) {
         // Two-Pass rows of a few blocks: one cluster per row, pass 2 from shared memory / L2
         if (A == kTwoPass && (o.schedule == 0 || o.schedule == 3)) {
-            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size);
+            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size, o.schedule == 0);
             if (CL) return launch_rowcl<In>(a, CL, o, s);
         }
         return launch_stream<In, A>(a, o, s);

@@ -215,7 +215,7 @@ int64_t lookahead_rows(const KArgs& a, int64_t grid, int items_per_cta, const La
 template <typename In, int A>
 cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s);
 template <typename In>
-int rowcl_choose(int64_t rows, int64_t nb, int force_cl);
+int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream);
 template <typename In>
 cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
 

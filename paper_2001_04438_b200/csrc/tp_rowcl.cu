@@ -566,7 +566,7 @@ static void rowcl_configure(int dev) {
 // time ~ rounds x (blocks per CTA + 1 for the row exchange); the L2 working set (pass-1 blocks
 // waiting for their pass-2 re-read, about half a row per cluster) must stay well inside L2.
 template <typename In>
-int rowcl_choose(int64_t rows, int64_t nb, int force_cl) {
+int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream) {
     if (nb < 2 || nb > kClMaxNb) return 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -588,7 +588,18 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl) {
         const double resident = (double)active * (double)(nb - (int64_t)CL * H > 0 ? nb - (int64_t)CL * H : 0) *
                                 block_bytes * 0.5;
         if (!force_cl && resident > 64e6) continue;
+        // automatic choice: the clusters must fill most of the GPU (a few long rows leave most
+        // SMs idle: the stream kernel spreads them over the whole grid instead)
+        if (!force_cl && vs_stream && active * CL * 4 < (int64_t)device_sms(dev) * 3) continue;
         if (best == 0 || t < best_t) best = CL, best_t = t;
+    }
+    if (best && vs_stream) {
+        // measured costs per block (pass 1 + pass 2) and CTA: cluster ~3.5 us per block of a
+        // CTA's share plus one block-time per row exchange; stream ~4.6 us per block over all SMs
+        // plus ~10 us of pass-1/pass-2 transition
+        const double t_cl = best_t * 3.5;
+        const double t_st = (double)rows * (double)nb / (double)device_sms(dev) * 4.6 + 10.0;
+        if (t_st < t_cl) return 0;
     }
     return best;
 }
@@ -633,8 +644,8 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, SA, LA);
 }
 
-template int rowcl_choose<float>(int64_t, int64_t, int);
-template int rowcl_choose<uint16_t>(int64_t, int64_t, int);
+template int rowcl_choose<float>(int64_t, int64_t, int, bool);
+template int rowcl_choose<uint16_t>(int64_t, int64_t, int, bool);
 template cudaError_t launch_rowcl<float>(KArgs, int, const LaunchOpts&, cudaStream_t);
 template cudaError_t launch_rowcl<uint16_t>(KArgs, int, const LaunchOpts&, cudaStream_t);
 

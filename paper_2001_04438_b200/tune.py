@@ -1,0 +1,103 @@
+"""Meta-parameter auto-tuner (the paper auto-tunes its kernels' unroll factor and
+accumulator count).
+
+The launch options that do not change results (include/twopass.h softmax_opts: schedule,
+cluster size, look-ahead, grid) are timed on the caller's own tensor shape and dtype, with the
+L2 flushed before every repetition, and the fastest set is cached per (device, dtype, rows,
+cols) in a JSON file.  `softmax_tuned` then launches with it.  Every candidate produces
+bit-identical outputs (tested), so tuning is safe to apply at any time.
+
+This is host-side orchestration only: every step of the method runs in libtwopass.so.
+"""
+from __future__ import annotations
+
+import json
+import os
+import threading
+
+import torch
+
+from . import (ALGO_TWO_PASS, SCHED_AUTO, SCHED_CLUSTER, SCHED_HOLD, SCHED_STREAM, softmax_ex)
+
+_LOCK = threading.Lock()
+DEFAULT_CACHE = os.path.join(os.path.expanduser("~"), ".cache", "paper_2001_04438_b200", "tune.json")
+
+
+def candidates(rows: int, cols: int) -> list[dict]:
+    """Launch-option sets worth timing for a shape (all valid; inapplicable ones fall back)."""
+    nb = (cols + 16383) // 16384
+    c = [dict(schedule=SCHED_AUTO), dict(schedule=SCHED_STREAM)]
+    if nb >= 2:
+        c += [dict(schedule=SCHED_STREAM, lookahead_rows=la) for la in (8, 16, 32) if la < rows]
+        c += [dict(schedule=SCHED_HOLD)]
+    if 2 <= nb <= 256:
+        c += [dict(schedule=SCHED_CLUSTER, cluster_size=cl) for cl in (1, 2, 4, 8) if cl <= nb]
+    return c
+
+
+def _key(x: torch.Tensor) -> str:
+    rows = x.numel() // x.shape[-1]
+    return f"{torch.cuda.get_device_name(x.device)}|{x.dtype}|{rows}|{x.shape[-1]}"
+
+
+def load_cache(path: str = DEFAULT_CACHE) -> dict:
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def save_cache(cache: dict, path: str = DEFAULT_CACHE) -> None:
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    tmp = path + ".tmp"
+    with open(tmp, "w") as f:
+        json.dump(cache, f, indent=1, sort_keys=True)
+    os.replace(tmp, path)
+
+
+def pick_best(timings: list[tuple[dict, float]]) -> dict:
+    """The option set with the smallest median time (ties: the earlier, simpler candidate)."""
+    best = min(range(len(timings)), key=lambda i: (timings[i][1], i))
+    return dict(timings[best][0])
+
+
+def time_options(x: torch.Tensor, opts: dict, reps: int = 5, flush_bytes: int = 512 << 20) -> float:
+    y = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    flush = torch.empty(flush_bytes, dtype=torch.uint8, device=x.device)
+    for _ in range(2):
+        softmax_ex(x, ALGO_TWO_PASS, out=y, **opts)
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        softmax_ex(x, ALGO_TWO_PASS, out=y, **opts)
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def tune(x: torch.Tensor, reps: int = 5, cache_path: str = DEFAULT_CACHE, force: bool = False) -> dict:
+    """Best launch options for x's shape and dtype (timed once, then cached)."""
+    key = _key(x)
+    with _LOCK:
+        cache = load_cache(cache_path)
+        if key in cache and not force:
+            return dict(cache[key]["opts"])
+    rows, cols = x.numel() // x.shape[-1], x.shape[-1]
+    timings = [(o, time_options(x, o, reps)) for o in candidates(rows, cols)]
+    best = pick_best(timings)
+    with _LOCK:
+        cache = load_cache(cache_path)
+        cache[key] = {"opts": best, "ms": min(t for _, t in timings),
+                      "timings": [{"opts": o, "ms": t} for o, t in timings]}
+        save_cache(cache, cache_path)
+    return best
+
+
+def softmax_tuned(x: torch.Tensor, out: torch.Tensor | None = None, cache_path: str = DEFAULT_CACHE) -> torch.Tensor:
+    """Two-Pass softmax with the tuned launch options for x's shape (tuning on first use)."""
+    return softmax_ex(x, ALGO_TWO_PASS, out=out, **tune(x, cache_path=cache_path))

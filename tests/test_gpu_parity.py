@@ -340,3 +340,16 @@ def test_host_pipeline_bf16_and_multi_slab():
     hx = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
     hy = tp.softmax_host(hx)
     assert_parity(x, hy.numpy(), "host bf16")
+
+
+def test_auto_tuner_picks_a_candidate_and_keeps_results_bitwise(tmp_path):
+    # NEXT-3 meta-parameter tuner: every candidate gives the same bits, so the tuned launch must too
+    from paper_2001_04438_b200 import tune
+    x = workloads.ragged_case(24, 16384 * 7 + 20, -300, 300, seed=12, stream=12)
+    xd = to_dev(x)
+    cache = str(tmp_path / "tune.json")
+    best = tune.tune(xd, reps=2, cache_path=cache)
+    assert best in tune.candidates(24, x.shape[1])
+    assert tune.tune(xd, cache_path=cache) == best            # cached
+    y = to_host(tune.softmax_tuned(xd, cache_path=cache))
+    assert np.array_equal(y, to_host(tp.softmax(xd)))
