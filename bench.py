@@ -230,6 +230,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-three-pass", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "nvlink"],
+                    help="rank merge of chunk-sharded rows: NCCL all_gather or one-sided NVLink mailboxes")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -273,9 +275,13 @@ def main():
     ws = tp.new_workspace(rows, cols, dev)
     stream = torch.cuda.current_stream(dev)
 
+    peer = None
+    if spec["mode"] == "chunk" and world > 1 and args.exchange == "nvlink":
+        peer = tpd.PeerPairExchange(rows, dev)
+
     def step_two_pass():
         if spec["mode"] == "chunk" and world > 1:
-            tpd.chunk_sharded_softmax(x, out=y, workspace=ws)
+            tpd.chunk_sharded_softmax(x, out=y, workspace=ws, exchange=peer)
         else:
             tp.softmax_ex(x, tp.ALGO_TWO_PASS, out=y, workspace=ws)
 
@@ -378,7 +384,9 @@ def main():
                        "l2": "inputs larger than L2 (no flush): %.0f MB/rank > 126 MB" %
                              (n_local * (4 if dtype == 'f32' else 2) / 1e6),
                        "parallelism": ("rows sharded, no collective" if spec["mode"] == "rows" else
-                                       "row chunk-sharded, one 8-byte (m,n) all_gather per rank")},
+                                       "row chunk-sharded, one 8-byte (m,n) per rank exchanged by " +
+                                       ("one-sided NVLink mailboxes" if args.exchange == "nvlink" else
+                                        "NCCL all_gather"))},
             "elements_per_s": elems_total / (ms_per_step * 1e-3),
             "pct_of_8TBs": value / world / NOMINAL_HBM_GBS if spec["scaling"] == "weak" else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -91,6 +91,33 @@ int softmax_f32_finish(const float* x, float* y, int64_t rows, int64_t cols, con
 int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t cols, const float* pairs,
                             int world, cudaStream_t stream);
 
+/* ---- one-sided pair exchange over NVLink (rank merge without a collective) --
+ * A mailbox (device memory of tp_mailbox_bytes(world, rows) bytes, owned by its rank, ZERO-
+ * FILLED once before first use) holds: bytes [0, 4*world) one uint32 flag per rank, bytes
+ * [240, 244) an error word (bit r: waiting for rank r timed out), and from byte 256 the pairs
+ * float[world][rows][2] (rank-major, the layout softmax_f32_finish takes).  world <= 56.
+ * tp_pairs_push: after softmax_*_partial on rank `rank`, stores its rows pairs (device) into
+ *   slot `rank` of every mailbox listed in peer_mailboxes (DEVICE array of world pointers,
+ *   entry p = rank p's mailbox mapped into this process: the local one, or one opened with
+ *   tp_ipc_open), then release-stores `epoch` into flag `rank` of each (system scope).
+ * tp_pairs_wait: on the local mailbox, waits until every flag equals `epoch` (acquire,
+ *   system scope), or timeout_ns elapsed (then sets the error word; outputs are undefined).
+ * Both asynchronous on `stream`; use a new epoch (e.g. 1, 2, ...) per exchange, the same on
+ * all ranks.  Then softmax_*_finish(x, y, rows, cols, mailbox + 256 bytes, world, ...).
+ * Sequence per rank: partial -> push -> wait -> finish; no NCCL, no host synchronisation.   */
+size_t tp_mailbox_bytes(int world, int64_t rows);
+int tp_pairs_push(const float* pairs, int64_t rows, void* const* peer_mailboxes, int rank, int world,
+                  unsigned epoch, cudaStream_t stream);
+int tp_pairs_wait(const void* mailbox, int world, unsigned epoch, uint64_t timeout_ns, cudaStream_t stream);
+/* CUDA IPC plumbing for the mailboxes (one process per GPU): tp_ipc_get_handle gives the
+ * 64-byte handle of the device allocation containing dev_ptr (made by this process, e.g. a
+ * caching-allocator segment) and dev_ptr's byte offset in it; tp_ipc_open maps a peer
+ * process's (handle, offset) into this process (peer access enabled lazily) and returns the
+ * pointer; tp_ipc_close unmaps a pointer tp_ipc_open returned.                              */
+int tp_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
+int tp_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);
+int tp_ipc_close(void* dev_ptr);
+
 /* ---- explicit-workspace / tuning variants ----------------------------------
  * workspace: device memory of at least softmax_workspace_bytes(rows, cols) bytes,
  *   ZERO-FILLED before its first use; the kernels leave it reusable.  One

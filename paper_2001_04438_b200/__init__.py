@@ -35,6 +35,7 @@ EXPORTS = [
     "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_f32_host", "softmax_bf16_f32_host",
     "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
     "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_exp_sweep", "tp_exp_fit",
+    "tp_mailbox_bytes", "tp_pairs_push", "tp_pairs_wait", "tp_ipc_get_handle", "tp_ipc_open", "tp_ipc_close",
 ]
 
 
@@ -87,6 +88,13 @@ def lib() -> ctypes.CDLL:
         L.softmax_watchdog_flags.argtypes = [vp, ci]
         L.tp_set_profile_buffer.argtypes = [vp]
         L.tp_exp_fit.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_uint32, i64, ci, vp, vp, vp]
+        L.tp_mailbox_bytes.argtypes = [ci, i64]
+        L.tp_mailbox_bytes.restype = sz
+        L.tp_pairs_push.argtypes = [vp, i64, vp, ci, ci, ctypes.c_uint, vp]
+        L.tp_pairs_wait.argtypes = [vp, ci, ctypes.c_uint, ctypes.c_uint64, vp]
+        L.tp_ipc_get_handle.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
+        L.tp_ipc_open.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]
+        L.tp_ipc_close.argtypes = [vp]
         L.tp_exp_sweep.argtypes = [ci, ctypes.c_uint32, i64, vp, vp, vp]
         L.tp_stream_baseline.argtypes = [ci, vp, vp, i64, ctypes.c_float, i64, vp]
         L.tp_bench_compute.argtypes = [ci, ci, i64, ci, vp, vp]

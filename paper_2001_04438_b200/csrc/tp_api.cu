@@ -2,6 +2,8 @@
 // the internal per-device workspace, the host-buffer (end-to-end) pipeline.  No arithmetic of
 // the method lives here; every step runs in the kernels of tp_kernels.cu.
 #include <cstring>
+
+#include <cuda.h>
 #include <mutex>
 #include <unordered_map>
 #include <utility>
@@ -317,6 +319,10 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
 
 }  // namespace
 
+// mapped pointer -> base of the IPC mapping it was opened from (tp_ipc_open / tp_ipc_close)
+std::mutex g_ipc_mu;
+std::unordered_map<void*, void*> g_ipc_base;
+
 extern "C" {
 
 int softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t stream) {
@@ -449,6 +455,78 @@ int tp_exp_fit(const float* coeffs, uint32_t bits0, int64_t count, int stride, u
         (uint64_t)bits0 + (uint64_t)count * (uint64_t)stride > 0x100000000ull)
         return TP_EINVAL;
     cudaError_t e = tp::launch_exp_fit(coeffs, bits0, count, stride, max_ulp_bits, n_over2, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+size_t tp_mailbox_bytes(int world, int64_t rows) {
+    return (world < 1 || world > 56 || rows < 0) ? 0 : tp::mailbox_bytes(world, rows);
+}
+
+int tp_pairs_push(const float* pairs, int64_t rows, void* const* peer_mailboxes, int rank, int world,
+                  unsigned epoch, cudaStream_t stream) {
+    if (!pairs || !peer_mailboxes || rows < 1 || world < 1 || world > 56 || rank < 0 || rank >= world)
+        return TP_EINVAL;
+    cudaError_t e = tp::launch_pairs_push(pairs, rows, peer_mailboxes, rank, world, epoch, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int tp_pairs_wait(const void* mailbox, int world, unsigned epoch, uint64_t timeout_ns, cudaStream_t stream) {
+    if (!mailbox || world < 1 || world > 56) return TP_EINVAL;
+    cudaError_t e = tp::launch_pairs_wait(mailbox, world, epoch, (unsigned long long)timeout_ns, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int tp_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset) {
+    if (!dev_ptr || !handle64 || !offset) return TP_EINVAL;
+    // the handle names the whole allocation (e.g. a caching-allocator segment): report where
+    // dev_ptr sits inside it
+    // driver entry point through the runtime (no link-time dependency on libcuda)
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<GetRange>(fn);
+    }();
+    if (!get_range) return TP_ECUDA;
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return TP_EINVAL;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return cuda_fail(e);
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle64, &h, sizeof(h));
+    *offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
+    return TP_OK;
+}
+
+int tp_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr) {
+    if (!handle64 || !dev_ptr) return TP_EINVAL;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e);
+    *dev_ptr = static_cast<char*>(base) + offset;
+    std::lock_guard<std::mutex> g(g_ipc_mu);
+    g_ipc_base[*dev_ptr] = base;
+    return TP_OK;
+}
+
+int tp_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return TP_EINVAL;
+    void* base = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_ipc_mu);
+        auto it = g_ipc_base.find(dev_ptr);
+        if (it == g_ipc_base.end()) return TP_EINVAL;
+        base = it->second;
+        g_ipc_base.erase(it);
+    }
+    cudaError_t e = cudaIpcCloseMemHandle(base);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 

@@ -64,6 +64,11 @@ cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, floa
 cudaError_t launch_exp_sweep(int what, uint32_t bits0, int64_t count, float* o0, float* o1, cudaStream_t s);
 cudaError_t launch_exp_fit(const float* c, uint32_t bits0, int64_t count, int stride, unsigned* max_bits,
                            unsigned long long* n_over2, cudaStream_t s);
+size_t mailbox_bytes(int world, int64_t rows);
+cudaError_t launch_pairs_push(const float* pairs, int64_t rows, void* const* mailboxes, int rank, int world,
+                              unsigned epoch, cudaStream_t s);
+cudaError_t launch_pairs_wait(const void* mailbox, int world, unsigned epoch, unsigned long long timeout_ns,
+                              cudaStream_t s);
 cudaError_t launch_bench_compute(int what, int in_bf16, int64_t ctas, int reps, float* sink, cudaStream_t s);
 
 }  // namespace tp

@@ -11,8 +11,13 @@ One process per GPU, torch.distributed for the plumbing.
     rank index inside the finish kernel (reading G8), so lambda_sum is bit-identical on all
     ranks and equal to the 1-GPU value; pass 2 then runs on the local chunk.
 
-The kernels are the library's (partial / finish through the C ABI); this module only
-partitions and exchanges.
+  * One-sided alternative: `PeerPairExchange` gives every rank a mailbox in
+    its own HBM, maps the peers' mailboxes through CUDA IPC once, and exchanges the pairs with
+    the library's push kernel (P2P stores over NVLink + release flags) and wait kernel
+    (acquire flags): no NCCL launch per call, no host synchronisation.
+
+The kernels are the library's (partial / finish / push / wait through the C ABI); this module
+only partitions and exchanges handles.
 """
 from __future__ import annotations
 
@@ -53,17 +58,105 @@ def exchange_pairs(local_pairs: torch.Tensor, group=None) -> torch.Tensor:
     return out.view(world, rows, 2)
 
 
+def gather_handles(local: bytes, group=None) -> list[bytes]:
+    """Every rank's IPC handle, rank-ordered (host plumbing; gloo or NCCL object collective)."""
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, local, group=group)
+    return out
+
+
+class PeerPairExchange:
+    """One-sided NVLink exchange of [rows, 2] pairs (include/twopass.h tp_pairs_push / wait).
+
+    `mailboxes` is normally None (one process per GPU: the mailboxes are shared with CUDA IPC
+    over `group`); a list of world mailbox tensors on one device runs world emulated ranks in
+    one process (tests: every push precedes every wait, so no kernel waits on another).
+    """
+
+    def __init__(self, rows: int, device, group=None, rank: int | None = None, world: int | None = None,
+                 mailboxes: list[torch.Tensor] | None = None, timeout_s: float = 5.0):
+        import ctypes
+
+        import paper_2001_04438_b200 as tp
+        self.tp, self.rows = tp, rows
+        self.world = world if world is not None else dist.get_world_size(group)
+        self.rank = rank if rank is not None else dist.get_rank(group)
+        L = tp.lib()
+        nbytes = int(L.tp_mailbox_bytes(self.world, rows))
+        if nbytes == 0:
+            raise ValueError("world must be 1..56")
+        self._opened = []
+        if mailboxes is not None:
+            self.mailbox = mailboxes[self.rank]
+            ptrs = [m.data_ptr() for m in mailboxes]
+        else:
+            self.mailbox = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+            h, off = ctypes.create_string_buffer(64), ctypes.c_uint64()
+            tp._check(L.tp_ipc_get_handle(self.mailbox.data_ptr(), h, ctypes.byref(off)), "tp_ipc_get_handle")
+            mine = h.raw + int(off.value).to_bytes(8, "little")
+            handles = gather_handles(mine, group) if self.world > 1 else [mine]
+            ptrs = []
+            for r, hr in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(self.mailbox.data_ptr())
+                    continue
+                p = ctypes.c_void_p()
+                tp._check(L.tp_ipc_open(hr[:64], int.from_bytes(hr[64:72], "little"), ctypes.byref(p)),
+                          "tp_ipc_open")
+                self._opened.append(p.value)
+                ptrs.append(p.value)
+        self.peer_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        self.epoch = 0
+        self.timeout_ns = int(timeout_s * 1e9)
+
+    def push(self, local_pairs: torch.Tensor, epoch: int) -> None:
+        tp = self.tp
+        tp._check(tp.lib().tp_pairs_push(local_pairs.data_ptr(), self.rows, self.peer_ptrs.data_ptr(), self.rank,
+                                         self.world, epoch, tp._stream()), "tp_pairs_push")
+
+    def wait(self, epoch: int) -> torch.Tensor:
+        """The [world, rows, 2] pairs of this epoch in the local mailbox (stream-ordered)."""
+        tp = self.tp
+        tp._check(tp.lib().tp_pairs_wait(self.mailbox.data_ptr(), self.world, epoch, self.timeout_ns,
+                                         tp._stream()), "tp_pairs_wait")
+        return self.pairs()
+
+    def pairs(self) -> torch.Tensor:
+        return self.mailbox[256:256 + 8 * self.world * self.rows].view(torch.float32).view(self.world, self.rows, 2)
+
+    def error(self) -> int:
+        """Bit r: the last waits timed out on rank r (reads device memory: synchronises)."""
+        return int(self.mailbox[240:244].view(torch.int32).item())
+
+    def exchange(self, local_pairs: torch.Tensor) -> torch.Tensor:
+        self.epoch += 1
+        self.push(local_pairs, self.epoch)
+        return self.wait(self.epoch)
+
+    def close(self) -> None:
+        for p in self._opened:
+            self.tp.lib().tp_ipc_close(p)
+        self._opened = []
+
+
 def chunk_sharded_softmax(x_chunk: torch.Tensor, out: torch.Tensor | None = None, group=None,
-                          workspace: torch.Tensor | None = None) -> torch.Tensor:
-    """Softmax of rows sharded by column chunk: partial -> all_gather(8 B/row/rank) -> finish."""
+                          workspace: torch.Tensor | None = None,
+                          exchange: "PeerPairExchange | None" = None) -> torch.Tensor:
+    """Softmax of rows sharded by column chunk: partial -> exchange 8 B/row/rank -> finish.
+
+    The exchange is one NCCL all_gather, or the one-sided NVLink mailboxes when `exchange` is
+    given."""
     import paper_2001_04438_b200 as tp
     rows = x_chunk.shape[0]
     if x_chunk.shape[-1] == 0:  # an empty trailing chunk contributes the identity (0, -inf)
         pairs = torch.tensor([[0.0, float("-inf")]] * rows, dtype=torch.float32, device=x_chunk.device)
-        exchange_pairs(pairs, group)
+        if exchange is not None:
+            exchange.exchange(pairs)
+        else:
+            exchange_pairs(pairs, group)
         return torch.empty(x_chunk.shape, dtype=torch.float32, device=x_chunk.device) if out is None else out
     pairs = tp.partial(x_chunk, workspace=workspace)
-    allp = exchange_pairs(pairs, group)
+    allp = exchange.exchange(pairs) if exchange is not None else exchange_pairs(pairs, group)
     return tp.finish(x_chunk, allp, allp.shape[0], out=out)
 
 

@@ -73,3 +73,32 @@ def test_pair_exchange_gloo_world2():
         assert p.exitcode == 0
     want = [[[w + 1.0, 10.0 * w + r] for r in range(3)] for w in range(world)]
     assert res[0] == want and res[1] == want           # every rank holds every pair, rank-major
+
+
+def _handles_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2001_04438_b200 import dist as tpd
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        q.put((rank, tpd.gather_handles(bytes([rank]) * 64)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_handles_gathered_rank_ordered():
+    # NEXT-4 plumbing: every rank sees every rank's 64-byte mailbox handle, in rank order
+    import multiprocessing as mp
+    import socket
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ps = [ctx.Process(target=_handles_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(2):
+        assert res[r] == [bytes([0]) * 64, bytes([1]) * 64]

@@ -1,0 +1,112 @@
+"""One-sided NVLink pair exchange (include/twopass.h tp_pairs_push / wait).
+
+One GPU here: W ranks are emulated on one device (every push precedes every wait, so no kernel
+waits on another kernel), and the CUDA IPC mapping is exercised with a second process that
+pushes into this process's mailbox and exits before this process waits.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from gpu_helpers import assert_parity, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_2001_04438_b200")
+from paper_2001_04438_b200 import dist as tpd  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _chunks(x, world):
+    return [x[:, slice(*tpd.chunk_range(x.shape[1], world, r))] for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("rows,cols", [(1, 16384 * 64), (3, 16384 * 8 + 96)])
+def test_mailbox_exchange_matches_allgather_and_one_gpu(world, rows, cols):
+    x = workloads.ragged_case(rows, cols, -1000, 1000, seed=21, stream=world)
+    xd = to_dev(x)
+    ref = to_host(tp.softmax(xd))
+    nbytes = tp.lib().tp_mailbox_bytes(world, rows)
+    boxes = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    ex = [tpd.PeerPairExchange(rows, "cuda", rank=r, world=world, mailboxes=boxes) for r in range(world)]
+    chunks = [c.contiguous() for c in _chunks(xd, world)]
+    ident = torch.tensor([[0.0, float("-inf")]] * rows, dtype=torch.float32, device="cuda")
+    for epoch in (1, 2):  # reuse without resetting the mailboxes
+        # an empty trailing chunk contributes the identity pair (dist.chunk_sharded_softmax)
+        parts = [tp.partial(c) if c.shape[1] else ident for c in chunks]
+        for r in range(world):
+            ex[r].push(parts[r], epoch)
+        outs = []
+        for r in range(world):
+            allp = ex[r].wait(epoch)
+            assert torch.equal(allp, torch.stack(parts))          # same bytes as an all_gather
+            if chunks[r].shape[1]:
+                outs.append(to_host(tp.finish(chunks[r], allp, world)))
+        y = np.concatenate(outs, axis=1)
+        assert all(e.error() == 0 for e in ex)
+        # power-of-two worlds over power-of-two block runs: bit-identical to one GPU (pin P9)
+        if cols % (16384 * world) == 0:
+            assert np.array_equal(y, ref)
+        else:
+            assert_parity(x, y, f"mailbox W={world}")
+
+
+def test_wait_times_out_instead_of_hanging():
+    ex = tpd.PeerPairExchange(2, "cuda", rank=0, world=2,
+                              mailboxes=[torch.zeros(tp.lib().tp_mailbox_bytes(2, 2), dtype=torch.uint8,
+                                                     device="cuda") for _ in range(2)], timeout_s=0.002)
+    ex.push(torch.zeros((2, 2), dtype=torch.float32, device="cuda"), 7)
+    ex.wait(7)                        # rank 1 never pushes
+    torch.cuda.synchronize()
+    assert ex.error() == 0b10
+
+
+CHILD = r"""
+import sys, ctypes, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2001_04438_b200 as tp, workloads
+from paper_2001_04438_b200 import dist as tpd
+handle = bytes.fromhex(sys.argv[2])
+offset = int(sys.argv[3])
+x = torch.from_numpy(workloads.ragged_case(2, 16384 * 4, -50, 50, seed=5, stream=5)).cuda()
+c1 = x[:, slice(*tpd.chunk_range(x.shape[1], 2, 1))].contiguous()
+p = ctypes.c_void_p()
+assert tp.lib().tp_ipc_open(handle, offset, ctypes.byref(p)) == 0
+mine = torch.zeros(tp.lib().tp_mailbox_bytes(2, 2), dtype=torch.uint8, device="cuda")
+peers = torch.tensor([p.value, mine.data_ptr()], dtype=torch.int64, device="cuda")
+pairs = tp.partial(c1)
+assert tp.lib().tp_pairs_push(pairs.data_ptr(), 2, peers.data_ptr(), 1, 2, 3, tp._stream()) == 0
+torch.cuda.synchronize()
+assert tp.lib().tp_ipc_close(p) == 0
+print("pushed")
+"""
+
+
+def test_ipc_mailbox_written_by_another_process():
+    import ctypes
+    x = workloads.ragged_case(2, 16384 * 4, -50, 50, seed=5, stream=5)
+    xd = to_dev(x)
+    box = torch.zeros(tp.lib().tp_mailbox_bytes(2, 2), dtype=torch.uint8, device="cuda")
+    h, off = ctypes.create_string_buffer(64), ctypes.c_uint64()
+    assert tp.lib().tp_ipc_get_handle(box.data_ptr(), h, ctypes.byref(off)) == 0
+    torch.cuda.synchronize()
+    r = subprocess.run([sys.executable, "-c", CHILD, ROOT, h.raw.hex(), str(off.value)], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "pushed" in r.stdout, r.stderr[-2000:]
+    ex = tpd.PeerPairExchange(2, "cuda", rank=0, world=2, mailboxes=[box, torch.zeros_like(box)])
+    c0 = xd[:, slice(*tpd.chunk_range(x.shape[1], 2, 0))].contiguous()
+    ex.push(tp.partial(c0), 3)
+    allp = ex.wait(3)
+    torch.cuda.synchronize()
+    assert ex.error() == 0
+    c1 = xd[:, slice(*tpd.chunk_range(x.shape[1], 2, 1))].contiguous()
+    assert torch.equal(allp[1], tp.partial(c1))                 # rank 1's pairs arrived through IPC
+    y = np.concatenate([to_host(tp.finish(c0, allp, 2)), to_host(tp.finish(c1, allp, 2))], axis=1)
+    assert np.array_equal(y, to_host(tp.softmax(xd)))
