@@ -133,7 +133,7 @@ int tp_ipc_close(void* dev_ptr);
  *   one thread-block cluster per row, the row's block values exchanged through distributed
  *   shared memory, pass 2 from shared memory / L2; AUTO picks it when the cluster's L2
  *   working set fits); a schedule that does not apply falls back to STREAM;
- *   cluster_size = CTAs per row for TP_SCHED_CLUSTER (0 = automatic; 1, 2, 4 or 8).
+ *   cluster_size = CTAs per row for TP_SCHED_CLUSTER (0 = automatic; 1, 2, 4, 8 or 16).
  *   Results do not depend on any of these (bit-identical outputs). */
 #define TP_SCHED_AUTO 0
 #define TP_SCHED_STREAM 1

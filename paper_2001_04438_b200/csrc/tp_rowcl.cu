@@ -524,8 +524,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
 // ----------------------------------------------------------------------------- host side
 template <typename In>
 static int max_active_clusters(int dev, int CL, size_t dyn) {
-    static int cache[64][4];
-    const int ci = CL == 1 ? 0 : CL == 2 ? 1 : CL == 4 ? 2 : 3;
+    static int cache[64][5];
+    const int ci = CL == 1 ? 0 : CL == 2 ? 1 : CL == 4 ? 2 : CL == 8 ? 3 : 4;
     if (cache[dev][ci]) return cache[dev][ci] > 0 ? cache[dev][ci] : 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(CL * 8));
@@ -558,6 +558,9 @@ static void rowcl_configure(int dev) {
     if (!configured[dev]) {
         cudaFuncSetAttribute(rowcl_kernel<In, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
         cudaFuncSetAttribute(rowcl_kernel<In, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
+        // clusters of 16 CTAs (non-portable; one per GPC on B200)
+        cudaFuncSetAttribute(rowcl_kernel<In, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(rowcl_kernel<In, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         configured[dev] = 1;
     }
 }
@@ -572,34 +575,36 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream) {
     cudaGetDevice(&dev);
     rowcl_configure<In>(dev);
     const size_t dyn = rowcl_dyn_smem<In>();
-    const double block_bytes = (double)kBlockElems * sizeof(In);
-    const int H = 0;  // no block stays staged between the passes
+    const int sms = device_sms(dev);
+    // Cost model (microseconds; constants measured on B200).  Compute: a
+    // CTA spends ~2.4 us per block of its share (both passes) plus one block-time per row for
+    // the exchange.  Memory: input + output + the pass-2 re-reads that miss L2, at ~6 TB/s; the
+    // miss fraction grows with the L2 footprint, about one row per active cluster (40 MB fit,
+    // 140 MB miss entirely).  The stream kernel: ~4.6 us per block over all SMs + ~10 us of
+    // pass-1/pass-2 transition, and all three passes of DRAM traffic.
+    const double in_b = (double)rows * (double)nb * kBlockElems * sizeof(In), out_b = (double)rows * nb * kBlockElems * 4.0;
     int best = 0;
     double best_t = 0.0;
-    for (int CL = 1; CL <= 8; CL *= 2) {
+    for (int CL = 1; CL <= 16; CL *= 2) {
         if (CL > nb || (nb + CL - 1) / CL > kClMaxLocal) continue;
         if (force_cl && CL != force_cl) continue;
         const int Q = max_active_clusters<In>(dev, CL, dyn);
         if (Q < 1) continue;
         const int64_t active = rows < Q ? rows : Q;
-        const int64_t rounds = (rows + Q - 1) / Q;
-        const int64_t per_cta = (nb + CL - 1) / CL;
-        const double t = (double)rounds * ((double)per_cta + 1.0);
-        const double resident = (double)active * (double)(nb - (int64_t)CL * H > 0 ? nb - (int64_t)CL * H : 0) *
-                                block_bytes * 0.5;
-        if (!force_cl && resident > 64e6) continue;
         // automatic choice: the clusters must fill most of the GPU (a few long rows leave most
         // SMs idle: the stream kernel spreads them over the whole grid instead)
-        if (!force_cl && vs_stream && active * CL * 4 < (int64_t)device_sms(dev) * 3) continue;
+        if (!force_cl && vs_stream && active * CL * 4 < (int64_t)sms * 3) continue;
+        const double per_cta = (double)((nb + CL - 1) / CL);
+        const double t_comp = ((double)rows / (double)Q) * (per_cta + 1.0) * 2.4;
+        const double foot = (double)active * (double)nb * kBlockElems * sizeof(In);
+        const double miss = fmin(1.0, fmax(0.0, (foot - 40e6) / 100e6));
+        const double t_mem = (in_b + out_b + miss * in_b) / 6.0e6;
+        const double t = fmax(t_comp, t_mem);
         if (best == 0 || t < best_t) best = CL, best_t = t;
     }
     if (best && vs_stream) {
-        // measured costs per block (pass 1 + pass 2) and CTA: cluster ~3.5 us per block of a
-        // CTA's share plus one block-time per row exchange; stream ~4.6 us per block over all SMs
-        // plus ~10 us of pass-1/pass-2 transition
-        const double t_cl = best_t * 3.5;
-        const double t_st = (double)rows * (double)nb / (double)device_sms(dev) * 4.6 + 10.0;
-        if (t_st < t_cl) return 0;
+        const double t_st = fmax((double)rows * (double)nb / (double)sms * 4.6 + 10.0, (2.0 * in_b + out_b) / 6.0e6);
+        if (t_st < best_t) return 0;
     }
     return best;
 }
