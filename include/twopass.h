@@ -195,7 +195,8 @@ int softmax_watchdog_flags(const void* workspace, int reset);
  *        1: pow2_flush(a) -> out0 = 2^a or 0 (a < -126, -inf, NaN)
  *        2: pair merge (a[2i], a[2i+1]) + (b[2i], b[2i+1]) -> (out0, out1)
  *        3: Exp with reconstruction, argument a <= 0 -> out0 (Alg. 4)
- *        4: the kernels' 2^k for integer k (MUFU.EX2, .ftz) -> out0              */
+ *        4: the kernels' 2^k for integer k (MUFU.EX2, .ftz) -> out0
+ *        5: %globaltimer (ns, uint64) into out0 viewed as uint64[count] (timeline marker) */
 int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                 cudaStream_t stream);
 

@@ -24,6 +24,7 @@ __global__ void debug_kernel(int what, const float* a, const float* b, float* o0
         }
         case 3: o0[i] = exp_flush2(make_float2(a[i], a[i])).x; break;
         case 4: o0[i] = ex2_ftz(a[i]); break;
+        case 5: reinterpret_cast<unsigned long long*>(o0)[i] = globaltimer_ns(); break;  // timeline marker
         default: break;
     }
 }

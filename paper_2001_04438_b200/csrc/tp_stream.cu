@@ -115,6 +115,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
     if (warp == kProducerWarp) {
         // =============================================================== producer warp
         if (lane != 0) return;
+        // development timeline (KArgs::prof): per CTA, globaltimer at start, at queue
+        // exhaustion and at exit, in prof[16 + 3 * blockIdx.x + {0, 1, 2}]
+        const unsigned long long tl_start = a.prof ? globaltimer_ns() : 0ull;
+        unsigned long long tl_exh = 0;
         const unsigned* row_ready = reinterpret_cast<const unsigned*>(a.ws + a.lay.row_ready);
         const In* x = static_cast<const In*>(a.x);
         const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
@@ -268,7 +272,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 }
                 if (state[s] == 0 && !exhausted) {
                     const long long item = take();
-                    if (item >= total) exhausted = true;
+                    if (item >= total) {
+                        exhausted = true;
+                        if (a.prof) tl_exh = globaltimer_ns();
+                    }
                     else issue(s, item);
                 }
                 busy |= state[s] != 0;
@@ -277,6 +284,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         }
         push(kOpExit, 0, 0);
         if (!hold && ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
+        if (a.prof) {
+            a.prof[16 + 3 * blockIdx.x] = tl_start;
+            a.prof[16 + 3 * blockIdx.x + 1] = tl_exh;
+            a.prof[16 + 3 * blockIdx.x + 2] = globaltimer_ns();
+        }
         exit_and_reset(hdr);
     } else if (warp == kRetireWarp) {
         // =============================================================== retire warp
