@@ -7,25 +7,25 @@
 // still be in L2: pass 2 re-reads HBM (12 B per element of DRAM traffic).  Here a cluster of CL
 // CTAs owns a row; each CTA streams its contiguous share of the row's blocks through pass 1,
 // the CTAs exchange their block values through distributed shared memory (one remote store
-// per block and one remote mbarrier arrive per CTA pair), and pass 2 starts a few microseconds
-// after the row's last load: the last H blocks of each CTA are still staged in shared memory
-// (read once), the others come back from L2.  DRAM traffic approaches the compulsory
-// 8 B per fp32 element (one read, one write).
+// per block and one remote mbarrier arrive per CTA pair), and pass 2 re-reads the row from L2
+// shortly after (backwards: most recently loaded first).  DRAM traffic approaches the
+// compulsory 8 B per fp32 element (one read, one write) when the rows in flight fit L2.
 //
-// Roles per CTA (18 warps, as the stream kernel): a producer warp (lane 0) walks the CTA's
-// fixed sequence of loads (pass 1 forward, pass 2 backward, row after row) into a ring of S
-// shared-memory stages with cp.async.bulk, and pushes one command per block op; 16 compute
-// warps execute the commands in order; warp 16+1 is idle.  Rows are assigned to clusters
-// round-robin (row = cluster id + k * clusters): no queue, no atomics.
+// Roles per CTA (19 warps): team A (warps 0-7) runs pass 1, team B (warps 8-15) pass 2;
+// producer A (warp 16, lane 0) streams the pass-1 loads into its half-stage pool, producer B
+// (warp 18) the pass-2 re-reads into its own; the tree warp (17) reduces each block's thread
+// pairs and does the row exchange and statistics.  Rows are assigned to clusters round-robin
+// (row = cluster id + k * clusters): no queue, no atomics.
 //
-// Results are bit-identical to the stream and general kernels: the same per-warp pass 1
-// (op_pass1), the same block tree over the 16 warp pairs, the same canonical group / row trees
-// (warp_reduce_leaves over the block values in block order, reading G8), the same pass 2.
+// Results are bit-identical to the stream and general kernels: the same per-thread pass 1
+// (thread_pass1), the same perfect tree over the block's 512 thread pairs (= the warp trees
+// then the tree over the 16 warps), the same canonical group / row trees over the block values
+// (reading G8), the same pass 2.
 //
-// Deadlock freedom: a CTA's pass 1 of a row depends only on its own loads, whose stages are
-// either released right after the copy to registers or held ones released by pass 2 of the
-// previous row, which (by induction over rows) got its cluster's statistics; so every CTA
-// finishes pass 1 of every row and every row barrier completes.
+// Deadlock freedom: team A's pass 1 of a row depends only on producer A's loads, which depend
+// on pool-A stages released by team A and on producer B having reached row k - LA; producer B
+// only needs pool-B stages, released by team B once the row's statistics exist, which needs
+// pass 1 of the row on every CTA of the cluster: by induction over rows every barrier completes.
 #include <cstdlib>
 
 #include "tp_ops.cuh"
@@ -66,8 +66,8 @@ __device__ __forceinline__ void load_half(const In* half, int wl, int lane, Bloc
     }
 }
 
-enum ClOp : int { kClP1 = 0, kClP1Hold = 1, kClP2 = 2, kClP2Held = 3, kClExit = 4 };
-enum ClFlag : int { kClLastP1 = 1, kClFirstP2 = 2 };
+enum ClOp : int { kClP1 = 0, kClP2 = 2, kClExit = 4 };
+enum ClFlag : int { kClFirstP2 = 2 };
 // development counters (KArgs::prof): clock cycles summed over CTAs
 enum ClProf : int {
     kProfCmdWait = 0, kProfFullWait, kProfRowWait, kProfP1, kProfP2, kProfComputeTotal,
@@ -75,11 +75,12 @@ enum ClProf : int {
 };
 
 struct ClCmd {
-    int op, stage;
-    unsigned parity;  // full[stage] parity of the load (loaded ops)
+    int op;
+    int stage;        // the block's half-stages and full-barrier parities: s0 | p0 << 4 | s1 << 5 | p1 << 9
+    unsigned unused;
     int k;            // row iteration of this cluster (row = cluster id + k * clusters)
-    int li;           // local block index (block = b_lo + li)
-    int flags;
+    int li;           // absolute block index in the row
+    int flags;        // kClFirstP2 | local block index << 8 (pass 2)
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
