@@ -245,13 +245,29 @@ def test_cluster_schedule_agrees_bitwise_with_stream(rows, cols, dtype):
         x = workloads.to_bf16(x)
     xd = to_dev(x)
     ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
-    for cl in [0, 1, 2, 4, 8]:
+    for cl in [0, 1, 2, 4, 8, 16]:
         y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_CLUSTER, cluster_size=cl))
         assert tp.watchdog_flags() == 0
         assert np.array_equal(ref, y), (cl, rows, cols)
     assert np.array_equal(ref, to_host(tp.softmax(xd)))
     if rows * cols <= 3_000_000:
         assert_parity(x, ref, "cluster")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_cluster_schedule_many_short_rows(dtype):
+    # thousands of rows of 2-3 blocks: every cluster loops over many rows (row parity buffers,
+    # epoch-free barriers), shares of 1-2 blocks per CTA
+    x = workloads.ragged_case(3000, 16384 * 2 + 1000, -80, 80, seed=13, stream=13)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    for cl in [0, 2, 3 - 1]:
+        y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_CLUSTER, cluster_size=cl))
+        assert tp.watchdog_flags() == 0
+        assert np.array_equal(ref, y), cl
+    assert_parity(x[:64], ref[:64], "many short rows")
 
 
 def test_cluster_schedule_clamped_blocks_and_small_grids():
