@@ -203,7 +203,7 @@ def cpu_baseline(args, spec):
 # ---------------------------------------------------------------- our arm
 
 KERNEL_NAMES = {"stream": "tp::stream_kernel<{In},kTwoPass>", "cluster": "tp::rowcl_kernel<{In}>",
-                "general": "tp::general_kernel<{In},kTwoPass>"}
+                "general": "tp::general_kernel<{In},kTwoPass>", "small": "tp::small_kernel<{In}>"}
 
 
 def traffic_from_profiles(workload: str, kernel: str):

@@ -139,6 +139,8 @@ int tp_ipc_close(void* dev_ptr);
 #define TP_SCHED_STREAM 1
 #define TP_SCHED_HOLD 2
 #define TP_SCHED_CLUSTER 3
+#define TP_SCHED_SMALL 4  /* rows of 1..3 blocks: one CTA per row, the row staged in shared
+                             memory (AUTO picks it for at most 2 x SMs such rows) */
 typedef struct {
     int64_t grid_ctas;
     int64_t lookahead_rows;
@@ -168,7 +170,7 @@ int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t c
 /* ---- status ---------------------------------------------------------------- */
 /* What the last launch issued by this host thread ran (diagnostics; no device work):
  * kernel = 1 general (any alignment), 2 stream (persistent grid), 3 cluster (one
- * thread-block cluster per row); variant = the kernel's operation (0 Two-Pass, 1 partial,
+ * thread-block cluster per row), 4 small (one CTA per row of <= 3 blocks); variant = the kernel's operation (0 Two-Pass, 1 partial,
  * 2 Recompute, 3 Reload, 4 single-block rows, 5 finish); grid_ctas; cluster_size (kernel 3);
  * lookahead_rows (kernel 1/2); hold = blocks kept staged between the passes (2: per row,
  * 3: per CTA and row).  Returns TP_EINVAL for a NULL pointer. */

@@ -25,7 +25,7 @@ _SO = os.environ.get("TP_LIBRARY") or os.path.join(_PKG, "libtwopass.so")
 
 TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV = 0, 1, 2, 3
 ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3
-SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER = 0, 1, 2, 3  # twopass.h TP_SCHED_*
+SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER, SCHED_SMALL = 0, 1, 2, 3, 4  # twopass.h TP_SCHED_*
 IN_F32, IN_BF16 = 0, 1
 
 EXPORTS = [
@@ -54,7 +54,7 @@ class SoftmaxPlan(ctypes.Structure):
                 ("cluster_size", ctypes.c_int), ("lookahead_rows", ctypes.c_int64), ("hold", ctypes.c_int)]
 
 
-KERNEL_NAMES = {0: "none", 1: "general", 2: "stream", 3: "cluster"}
+KERNEL_NAMES = {0: "none", 1: "general", 2: "stream", 3: "cluster", 4: "small"}
 
 _lib = None
 

@@ -270,6 +270,25 @@ def test_cluster_schedule_many_short_rows(dtype):
     assert_parity(x[:64], ref[:64], "many short rows")
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", [(1, 1000), (7, 16384), (64, 32768), (3, 16384 * 3), (5, 16384 * 2 + 36),
+                                       (400, 16384 * 2 + 4)])
+def test_small_schedule_agrees_bitwise(rows, cols, dtype):
+    # one CTA per row of <= 3 blocks, row staged in shared memory (tp_small.cu); 400 rows loop
+    x = workloads.ragged_case(rows, cols, -300, 300, seed=14, stream=rows + cols)
+    x[0, 3] = 4.0e7 if rows > 1 else x[0, 3]       # one out-of-domain block (clamped path)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_SMALL))
+    if cols % (8 if dtype == "bf16" else 4) == 0:       # 16-byte rows; others take the general kernel
+        assert tp.last_plan()["kernel"] == "small"
+    assert np.array_equal(ref, y)
+    if rows * cols <= 3_000_000 and rows > 1:
+        assert_parity(x[1:], y[1:], "small")
+
+
 def test_cluster_schedule_clamped_blocks_and_small_grids():
     # out-of-domain blocks (reading G11) inside multi-block rows: the per-warp clamp masks stay
     # local to the CTA that ran pass 1; a capped grid makes clusters loop over many rows
