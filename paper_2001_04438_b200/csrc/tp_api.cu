@@ -1,6 +1,7 @@
 // C ABI of libtwopass.so (declared and documented in include/twopass.h): argument checks,
 // the internal per-device workspace, the host-buffer (end-to-end) pipeline.  No arithmetic of
 // the method lives here; every step runs in the kernels of tp_kernels.cu.
+#include <cstdlib>
 #include <cstring>
 
 #include <cuda.h>
@@ -21,16 +22,20 @@ int cuda_fail(cudaError_t e) {
 }
 
 constexpr int kMaxDev = 64;
+constexpr int kHostStreams = 4;                // host pipeline: stream slots (default use: 2)
+constexpr size_t kHostSlabBytes = 64ull << 20;  // host pipeline: input bytes per slab
+// Measured on B200 (tools/pcie_probe.py, C4): H2D 14.8 ms and D2H 15.2 ms alone, 17.0 ms at
+// once; 2 streams x 64 MB slabs 18.1 ms end to end; smaller slabs or more streams are slower.
 
 struct DevState {
     std::mutex mu;
     void* ws = nullptr;
     size_t ws_bytes = 0;
-    // host pipeline, row slabs: two staging slots (one per stream)
-    void* hx_dev[2] = {nullptr, nullptr};
-    float* hy_dev[2] = {nullptr, nullptr};
+    // host pipeline, row slabs: one staging slot per stream
+    void* hx_dev[kHostStreams] = {};
+    float* hy_dev[kHostStreams] = {};
     size_t stage_bytes_x = 0, stage_bytes_y = 0;
-    void* hws[2] = {nullptr, nullptr};
+    void* hws[kHostStreams] = {};
     size_t hws_bytes = 0;
     // host pipeline, single long row: whole-row buffers, chunk workspace, chunk pairs
     void* row_x = nullptr;
@@ -40,7 +45,7 @@ struct DevState {
     size_t row_ws_bytes = 0;
     void* pairs = nullptr;
     size_t pairs_bytes = 0;
-    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaStream_t st[kHostStreams] = {};
     cudaEvent_t ev[64];
     bool ev_init = false;
 };
@@ -199,7 +204,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
     std::lock_guard<std::mutex> lk(d.mu);
     cudaError_t e;
     if (!d.st[0]) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostStreams; ++i) {
             e = cudaStreamCreateWithFlags(&d.st[i], cudaStreamNonBlocking);
             if (e != cudaSuccess) return cuda_fail(e);
         }
@@ -255,15 +260,27 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         return e == cudaSuccess ? TP_OK : cuda_fail(e);
     }
 
-    // Row slabs, double-buffered over two streams: H2D(slab i+1) overlaps kernel + D2H(slab i).
-    int64_t slab = (int64_t)((64ull << 20) / ((size_t)cols * 4));
+    // Row slabs of ~64 MB round-robin over 2 streams: the H2D copy of the next slab, the kernel
+    // and the D2H copy of the previous slab overlap (the two copy directions run concurrently,
+    // so the pipeline approaches the bidirectional PCIe rate).
+    static const size_t slab_bytes = [] {  // development override TP_HOST_SLAB_MB
+        const char* e = getenv("TP_HOST_SLAB_MB");
+        return e ? (size_t)atoi(e) << 20 : kHostSlabBytes;
+    }();
+    static const int nstreams = [] {  // development override TP_HOST_STREAMS (1..kHostStreams)
+        const char* e = getenv("TP_HOST_STREAMS");
+        const int v = e ? atoi(e) : 2;
+        return v < 1 ? 1 : (v > kHostStreams ? kHostStreams : v);
+    }();
+    int64_t slab = (int64_t)(slab_bytes / ((size_t)cols * esz));
     if (slab < 1) slab = 1;
     if (slab > rows) slab = rows;
     const size_t need_x = (size_t)(slab * cols) * esz, need_y = (size_t)(slab * cols) * 4;
-    if (d.stage_bytes_x < need_x || d.stage_bytes_y < need_y || !d.hx_dev[1] || !d.hy_dev[1]) {
+    if (d.stage_bytes_x < need_x || d.stage_bytes_y < need_y || !d.hx_dev[kHostStreams - 1] ||
+        !d.hy_dev[kHostStreams - 1]) {
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostStreams; ++i) {
             if (d.hx_dev[i]) cudaFree(d.hx_dev[i]);
             if (d.hy_dev[i]) cudaFree(d.hy_dev[i]);
             d.hx_dev[i] = nullptr;
@@ -271,7 +288,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         }
         const size_t bx = need_x > d.stage_bytes_x ? need_x : d.stage_bytes_x;
         const size_t by = need_y > d.stage_bytes_y ? need_y : d.stage_bytes_y;
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostStreams; ++i) {
             if ((e = cudaMalloc(&d.hx_dev[i], bx)) != cudaSuccess) return cuda_fail(e);
             if ((e = cudaMalloc((void**)&d.hy_dev[i], by)) != cudaSuccess) return cuda_fail(e);
         }
@@ -282,10 +299,10 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
     const bool needs_ws = tp::softmax_needs_workspace(TP_ALGO_TWO_PASS, cols, lo);
     if (needs_ws) {
         const size_t wsb = tp::workspace_bytes(slab, cols);
-        if (d.hws_bytes < wsb || !d.hws[1]) {
+        if (d.hws_bytes < wsb || !d.hws[kHostStreams - 1]) {
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return cuda_fail(e);
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < kHostStreams; ++i) {
                 if (d.hws[i]) {
                     cudaFree(d.hws[i]);
                     forget_ws(d.hws[i]);
@@ -297,7 +314,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         }
     }
     for (int64_t r0 = 0, i = 0; r0 < rows; r0 += slab, ++i) {
-        const int k = (int)(i & 1);
+        const int k = (int)(i % nstreams);
         const int64_t nr = rows - r0 < slab ? rows - r0 : slab;
         cudaStream_t s = d.st[k];
         e = cudaMemcpyAsync(d.hx_dev[k], (const char*)hx + (size_t)(r0 * cols) * esz, (size_t)(nr * cols) * esz,
@@ -310,7 +327,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         e = cudaMemcpyAsync(hy + (size_t)(r0 * cols), d.hy_dev[k], (size_t)(nr * cols) * 4, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_fail(e);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kHostStreams; ++i) {
         e = cudaStreamSynchronize(d.st[i]);
         if (e != cudaSuccess) return cuda_fail(e);
     }
