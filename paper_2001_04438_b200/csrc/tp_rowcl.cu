@@ -577,12 +577,14 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream) {
     rowcl_configure<In>(dev);
     const size_t dyn = rowcl_dyn_smem<In>();
     const int sms = device_sms(dev);
-    // Cost model (microseconds; constants measured on B200).  Compute: a
-    // CTA spends ~2.4 us per block of its share (both passes) plus one block-time per row for
-    // the exchange.  Memory: input + output + the pass-2 re-reads that miss L2, at ~6 TB/s; the
-    // miss fraction grows with the L2 footprint, about one row per active cluster (40 MB fit,
-    // 140 MB miss entirely).  The stream kernel: ~4.6 us per block over all SMs + ~10 us of
-    // pass-1/pass-2 transition, and all three passes of DRAM traffic.
+    // Cost model (microseconds; constants measured on B200).  Pipeline: a
+    // CTA spends ~3.1 us per block of its share (both passes, either dtype: the two 8-warp
+    // teams' latency, not the arithmetic, sets it) plus one block-time per row for the
+    // exchange.  Memory: input + output + the pass-2 re-reads that miss L2, at ~6 TB/s; the miss
+    // fraction grows with the L2 footprint, about one row per active cluster (40 MB fit,
+    // 140 MB miss entirely).  The stream kernel: ~4.6 us per block over all SMs (its pipeline:
+    // C4 fp32 392 us, bf16 419 us) + ~10 us of pass-1/pass-2 transition, or its DRAM traffic
+    // (input twice + output) at ~6 TB/s.
     const double in_b = (double)rows * (double)nb * kBlockElems * sizeof(In), out_b = (double)rows * nb * kBlockElems * 4.0;
     int best = 0;
     double best_t = 0.0;
@@ -596,7 +598,7 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream) {
         // SMs idle: the stream kernel spreads them over the whole grid instead)
         if (!force_cl && vs_stream && active * CL * 4 < (int64_t)sms * 3) continue;
         const double per_cta = (double)((nb + CL - 1) / CL);
-        const double t_comp = ((double)rows / (double)Q) * (per_cta + 1.0) * 2.4;
+        const double t_comp = ((double)rows / (double)Q) * (per_cta + 1.0) * 3.1;
         const double foot = (double)active * (double)nb * kBlockElems * sizeof(In);
         const double miss = fmin(1.0, fmax(0.0, (foot - 40e6) / 100e6));
         const double t_mem = (in_b + out_b + miss * in_b) / 6.0e6;

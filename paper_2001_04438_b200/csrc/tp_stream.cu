@@ -132,16 +132,19 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         }
         bool exhausted = false;
         long long pushed = 0;
-        unsigned use[S];       // issues of each stage so far
-        int state[S];          // 0 free, 1 busy (until its empty barrier completes), 2 waiting for stats,
-                               // 3 retired (hold mode: its reservation was past the end)
+        // per stage, in registers: parity of the next use (bit s of use_par), state (2 bits: 0 free,
+        // 1 busy until its empty barrier completes, 2 waiting for stats, 3 retired (hold mode:
+        // its reservation was past the end)), issue sequence of its item (order[], local)
+        unsigned use_par = 0, st_bits = 0;
+        auto state_of = [&](int s) -> int { return (int)((st_bits >> (2 * s)) & 3u); };
+        auto set_state = [&](int s, int v) { st_bits = (st_bits & ~(3u << (2 * s))) | ((unsigned)v << (2 * s)); };
         long long order[S];    // issue sequence of the stage's item (stats are provided in this order)
         // hold mode: each stage owns one reservation, taken when the stage is certain to free
         // without waiting on anything (at start, and when its P2 command is pushed).  A CTA
         // never reserves a block it cannot stage, so the oldest unreleased row always gets all
         // its blocks staged (a row must not wait on a block queued behind held stages).
         unsigned long long resv[S];
-        for (int s = 0; s < S; ++s) use[s] = 0, state[s] = 0, order[s] = 0;
+        for (int s = 0; s < S; ++s) order[s] = 0;
         if (hold)
             for (int s = 0; s < S; ++s) resv[s] = atomicAdd(&hdr->counter, 1ull);
         long long issue_seq = 0;
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             for (;;) {
                 int best = -1;
                 for (int s = 0; s < S; ++s)
-                    if (state[s] == 2 && (best < 0 || order[s] < order[best])) best = s;
+                    if (state_of(s) == 2 && (best < 0 || order[s] < order[best])) best = s;
                 if (best < 0) return;
                 const Item it = meta[best].it;
                 float4 st;
@@ -201,8 +204,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                                       ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) +
                                                it.row * a.nb + it.blk)
                                       : 0u;
-                state[best] = 1;
-                push(hold ? kOpP2 : kOpItem, best, (use[best] - 1) & 1u);
+                set_state(best, 1);
+                push(hold ? kOpP2 : kOpItem, best, ((use_par >> best) & 1u) ^ 1u);
                 if (hold) resv[best] = atomicAdd(&hdr->counter, 1ull);  // consumed when the stage frees
             }
         };
@@ -222,8 +225,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             meta[s].item = item;
             meta[s].it = it;
             meta[s].valid = valid;
-            const unsigned parity = use[s] & 1u;
-            ++use[s];
+            const unsigned parity = (use_par >> s) & 1u;
+            use_par ^= 1u << s;
             order[s] = issue_seq++;
             if (A == kReload && it.phase == 2) {  // Reload's pass 3 reads Y, not X: no copy
                 mbar_arrive(&full_bar[s]);
@@ -245,13 +248,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 meta[s].mask = 0xffffffffu;  // the chunk's pass-1 clamp decisions are not known here
             }
             if (hold) {
-                state[s] = 2;  // P1 now, P2 once the row is released
+                set_state(s, 2);  // P1 now, P2 once the row is released
                 push(kOpP1, s, parity);
             } else if (item_needs_stats<A>(it) && A != kFinish) {
-                state[s] = 2;
+                set_state(s, 2);
                 poll();
             } else {
-                state[s] = 1;
+                set_state(s, 1);
                 push(kOpItem, s, parity);
             }
         };
@@ -261,16 +264,16 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             poll();
             bool busy = false;
             for (int s = 0; s < S; ++s) {
-                if (state[s] == 1 && mbar_test_parity(&empty_bar[s], (use[s] - 1) & 1u)) state[s] = 0;
+                if (state_of(s) == 1 && mbar_test_parity(&empty_bar[s], ((use_par >> s) & 1u) ^ 1u)) set_state(s, 0);
                 if (hold) {
-                    if (state[s] == 0) {
-                        if (resv[s] >= (unsigned long long)total) state[s] = 3;
+                    if (state_of(s) == 0) {
+                        if (resv[s] >= (unsigned long long)total) set_state(s, 3);
                         else issue(s, (long long)resv[s]);
                     }
-                    busy |= state[s] != 3;
+                    busy |= state_of(s) != 3;
                     continue;
                 }
-                if (state[s] == 0 && !exhausted) {
+                if (state_of(s) == 0 && !exhausted) {
                     const long long item = take();
                     if (item >= total) {
                         exhausted = true;
@@ -278,9 +281,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                     }
                     else issue(s, item);
                 }
-                busy |= state[s] != 0;
+                busy |= state_of(s) != 0;
             }
             if ((hold || exhausted) && !busy) break;
+
         }
         push(kOpExit, 0, 0);
         if (!hold && ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
