@@ -388,3 +388,23 @@ def test_auto_tuner_picks_a_candidate_and_keeps_results_bitwise(tmp_path):
     assert tune.tune(xd, cache_path=cache) == best            # cached
     y = to_host(tune.softmax_tuned(xd, cache_path=cache))
     assert np.array_equal(y, to_host(tp.softmax(xd)))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("algo", list(ALGOS))
+@pytest.mark.parametrize("grid", [1, 4, 0])
+def test_fresh_workspace_small_grids_repeated(algo, dtype, grid):
+    # regression: the stream kernel's producer once stalled after one round of stages for bf16
+    # Three-Pass Recompute on a fresh workspace (stage bookkeeping in local arrays); every
+    # algorithm, dtype and grid size on a fresh workspace, three launches, watchdog clear
+    x = workloads.ragged_case(3, 16384 * 10 + 96, -200, 200, seed=15, stream=grid)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    ws = tp.new_workspace(*x.shape)
+    ys = []
+    for _ in range(3):
+        ys.append(to_host(tp.softmax_ex(xd, ALGOS[algo], workspace=ws, grid_ctas=grid, schedule=tp.SCHED_STREAM)))
+        assert tp.watchdog_flags(ws) == 0
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
+    assert_parity(x, ys[0], f"{algo}/{dtype}/grid {grid}")
