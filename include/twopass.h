@@ -119,7 +119,8 @@ int tp_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);
 int tp_ipc_close(void* dev_ptr);
 
 /* ---- explicit-workspace / tuning variants ----------------------------------
- * workspace: device memory of at least softmax_workspace_bytes(rows, cols) bytes,
+ * workspace: device memory of at least softmax_workspace_bytes(rows, cols) bytes (it includes
+ *   a second layout for the tail rows a cluster launch may hand to a concurrent launch),
  *   ZERO-FILLED before its first use; the kernels leave it reusable.  One
  *   workspace must not be used by two launches running concurrently.
  * opts: may be NULL.  grid_ctas = persistent grid size (0 = one resident wave;
@@ -172,8 +173,9 @@ int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t c
  * kernel = 1 general (any alignment), 2 stream (persistent grid), 3 cluster (one
  * thread-block cluster per row), 4 small (one CTA per row of <= 3 blocks); variant = the kernel's operation (0 Two-Pass, 1 partial,
  * 2 Recompute, 3 Reload, 4 single-block rows, 5 finish); grid_ctas; cluster_size (kernel 3);
- * lookahead_rows (kernel 1/2); hold = blocks kept staged between the passes (2: per row,
- * 3: per CTA and row).  Returns TP_EINVAL for a NULL pointer. */
+ * lookahead_rows (kernel 1/2; kernel 3: rows handed to a concurrent stream launch on the SMs
+ * the clusters leave idle, 0 if none); hold (kernel 2: blocks kept staged between the passes;
+ * kernel 3: half-stages of the pass-1 pool).  Returns TP_EINVAL for a NULL pointer. */
 typedef struct {
     int kernel;
     int variant;

@@ -72,6 +72,8 @@ int prepare_ws(void* ws, int64_t rows, int64_t cols, cudaStream_t s) {
         g_ws_shape[ws] = std::make_pair(rows, cols);
     }
     cudaError_t e = cudaMemsetAsync(ws, 0, tp::workspace_ctrl_bytes(rows, cols), s);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync((char*)ws + tp::tail_ws_offset(rows, cols), 0, tp::tail_ctrl_bytes(rows, cols), s);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 
@@ -428,14 +430,25 @@ int softmax_watchdog_flags(const void* workspace, int reset) {
         ws = g_dev[dev].ws;
         if (!ws) return 0;
     }
-    tp::WsHeader h;
+    // the main header, and the tail layout's header (a concurrent tail launch), found through
+    // the shape the workspace was last prepared for
+    size_t toff = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_shape_mu);
+        auto it = g_ws_shape.find(ws);
+        if (it != g_ws_shape.end()) toff = tp::tail_ws_offset(it->second.first, it->second.second);
+    }
+    tp::WsHeader h, ht{};
     if (cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    if (reset && h.error) {
-        forget_ws(ws);  // the aborted launch may have left tickets behind: re-zero on next use
+    if (toff && cudaMemcpy(&ht, (const char*)ws + toff, sizeof(ht), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    const unsigned err = h.error | ht.error;
+    if (reset && err) {
         unsigned z = 0;
         cudaMemcpy((char*)ws + offsetof(tp::WsHeader, error), &z, sizeof(z), cudaMemcpyHostToDevice);
+        if (toff) cudaMemcpy((char*)ws + toff + offsetof(tp::WsHeader, error), &z, sizeof(z), cudaMemcpyHostToDevice);
+        forget_ws(ws);  // the aborted launch may have left tickets behind: re-zero on next use
     }
-    return (int)h.error;
+    return (int)err;
 }
 
 int tp_set_profile_buffer(void* p) {

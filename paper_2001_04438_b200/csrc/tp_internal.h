@@ -49,6 +49,9 @@ size_t workspace_bytes(int64_t rows, int64_t cols);
 // The control region's layout depends on (rows, cols): it must be re-zeroed whenever a
 // workspace is used with a different shape than its previous launch (tp_api.cu does that).
 size_t workspace_ctrl_bytes(int64_t rows, int64_t cols);
+// the tail layout of a workspace (a concurrent launch on a cluster launch's last rows)
+size_t tail_ws_offset(int64_t rows, int64_t cols);
+size_t tail_ctrl_bytes(int64_t rows, int64_t cols);
 bool softmax_needs_workspace(int algo, int64_t cols, const LaunchOpts& o);
 cudaError_t launch_softmax(int algo, int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, void* ws,
                            const LaunchOpts& o, cudaStream_t s);

@@ -16,13 +16,23 @@
 // that order, and an item depends only on items of smaller index; so the smallest unfinished
 // item is always the current item of a running CTA.
 #include <cstdlib>
+#include <mutex>
 
 #include "tp_ops.cuh"
 
 namespace tp {
 
-size_t workspace_bytes(int64_t rows, int64_t cols) { return ws_layout(rows, cols).bytes; }
+// After the main layout: a second layout for up to kMaxTailRows rows that a concurrent stream
+// launch (launch_split) uses for the tail rows of a cluster launch.
+constexpr int64_t kMaxTailRows = 256;
+size_t tail_ws_offset(int64_t rows, int64_t cols) { return align256(ws_layout(rows, cols).bytes); }
+size_t workspace_bytes(int64_t rows, int64_t cols) {
+    return tail_ws_offset(rows, cols) + ws_layout(rows < kMaxTailRows ? rows : kMaxTailRows, cols).bytes;
+}
 size_t workspace_ctrl_bytes(int64_t rows, int64_t cols) { return ws_layout(rows, cols).ctrl_bytes; }
+size_t tail_ctrl_bytes(int64_t rows, int64_t cols) {
+    return ws_layout(rows < kMaxTailRows ? rows : kMaxTailRows, cols).ctrl_bytes;
+}
 
 template <typename In, int A>
 __global__ void __launch_bounds__(kThreads, 1) general_kernel(const KArgs a) {
@@ -176,6 +186,55 @@ static cudaError_t launch_general(KArgs a, const LaunchOpts& o, cudaStream_t s) 
     return cudaGetLastError();
 }
 
+// Cluster kernel on the first rows - tail rows, the stream kernel on the tail rows on the SMs the
+// clusters leave idle, concurrently: fork / join on an internal side stream with events (graph
+// capturable).  The tail uses the workspace's tail layout (tail_ws_offset).
+// cudaErrorNotSupported for a tail longer than that layout: the caller runs the plain launch.
+
+struct SideStream {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream g_side[64];
+
+template <typename In>
+static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_ctas, const LaunchOpts& o,
+                                cudaStream_t s) {
+    if (tail > kMaxTailRows) return cudaErrorNotSupported;
+    const WsLayout lt = ws_layout(tail, a.cols);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SideStream& ss = g_side[dev];
+    std::lock_guard<std::mutex> lk(ss.mu);
+    cudaError_t e;
+    if (!ss.st) {
+        if ((e = cudaStreamCreateWithFlags(&ss.st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    KArgs main = a, t = a;
+    main.rows = a.rows - tail;
+    main.total_items = main.rows * a.nb;
+    t.rows = tail;
+    t.total_items = tail * a.nb * AlgoTraits<kTwoPass>::P;
+    t.x = static_cast<const In*>(a.x) + main.rows * a.cols;
+    t.y = a.y + main.rows * a.cols;
+    t.ws = a.ws + tail_ws_offset(a.rows, a.cols);
+    t.lay = lt;
+    LaunchOpts ot = o;
+    ot.grid_ctas = tail_ctas;
+    ot.schedule = 1;
+    if ((e = cudaEventRecord(ss.fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ss.st, ss.fork, 0)) != cudaSuccess) return e;
+    if ((e = launch_rowcl<In>(main, CL, o, s)) != cudaSuccess) return e;  // clusters first: they need whole GPCs
+    const Plan p = last_plan();
+    if ((e = launch_stream<In, kTwoPass>(t, ot, ss.st)) != cudaSuccess) return e;
+    last_plan() = Plan{p.kernel, p.variant, p.grid_ctas, p.cluster_size, (int64_t)tail, p.hold};
+    if ((e = cudaEventRecord(ss.join, ss.st)) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(s, ss.join, 0);
+}
+
 template <typename In, int A>
 static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t cols, void* ws, float2* pair_out,
                                const float2* pairs_in, int world, const LaunchOpts& o, cudaStream_t s) {
@@ -203,7 +262,13 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
             return launch_small<In>(a, o, s);
         // Two-Pass rows of a few blocks: one cluster per row, pass 2 from shared memory / L2
         if (A == kTwoPass && (o.schedule == 0 || o.schedule == 3)) {
-            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size, o.schedule == 0);
+            int64_t tail = 0;
+            int tail_ctas = 0;
+            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size, o.schedule == 0, &tail, &tail_ctas);
+            if (CL && tail > 0) {
+                const cudaError_t e = launch_split<In>(a, CL, tail, tail_ctas, o, s);
+                if (e != cudaErrorNotSupported) return e;
+            }
             if (CL) return launch_rowcl<In>(a, CL, o, s);
         }
         return launch_stream<In, A>(a, o, s);

@@ -218,7 +218,7 @@ bool small_applies(int64_t rows, int64_t nb, int vec);
 template <typename In>
 cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s);
 template <typename In>
-int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream);
+int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t* tail_rows, int* tail_ctas);
 template <typename In>
 cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
 

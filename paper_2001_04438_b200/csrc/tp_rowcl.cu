@@ -570,7 +570,9 @@ static void rowcl_configure(int dev) {
 // time ~ rounds x (blocks per CTA + 1 for the row exchange); the L2 working set (pass-1 blocks
 // waiting for their pass-2 re-read, about half a row per cluster) must stay well inside L2.
 template <typename In>
-int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream) {
+int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t* tail_rows, int* tail_ctas) {
+    *tail_rows = 0;
+    *tail_ctas = 0;
     if (nb < 2 || nb > kClMaxNb) return 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -578,9 +580,9 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream) {
     const size_t dyn = rowcl_dyn_smem<In>();
     const int sms = device_sms(dev);
     // Cost model (microseconds; constants measured on B200).  Pipeline: a
-    // CTA spends ~3.1 us per block of its share (both passes, either dtype: the two 8-warp
-    // teams' latency, not the arithmetic, sets it) plus one block-time per row for the
-    // exchange.  Memory: input + output + the pass-2 re-reads that miss L2, at ~6 TB/s; the miss
+    // CTA spends ~2.5 us per block of its share (both passes; the two 8-warp teams' latency,
+    // not the arithmetic, sets it), up to ~3.5 us when the re-reads miss L2, plus one block-time
+    // per row for the exchange.  Memory: input + output + the pass-2 re-reads that miss L2, at ~6 TB/s; the miss
     // fraction grows with the L2 footprint, about one row per active cluster (40 MB fit,
     // 140 MB miss entirely).  The stream kernel: ~4.6 us per block over all SMs (its pipeline:
     // C4 fp32 392 us, bf16 419 us) + ~10 us of pass-1/pass-2 transition, or its DRAM traffic
@@ -598,16 +600,38 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream) {
         // SMs idle: the stream kernel spreads them over the whole grid instead)
         if (!force_cl && vs_stream && active * CL * 4 < (int64_t)sms * 3) continue;
         const double per_cta = (double)((nb + CL - 1) / CL);
-        const double t_comp = ((double)rows / (double)Q) * (per_cta + 1.0) * 3.1;
         const double foot = (double)active * (double)nb * kBlockElems * sizeof(In);
         const double miss = fmin(1.0, fmax(0.0, (foot - 40e6) / 100e6));
+        const double per_round = (per_cta + 1.0) * (2.5 + 1.0 * miss);
         const double t_mem = (in_b + out_b + miss * in_b) / 6.0e6;
-        const double t = fmax(t_comp, t_mem);
-        if (best == 0 || t < best_t) best = CL, best_t = t;
+        const int64_t full = rows / Q, rem = rows - full * Q;
+        double t = fmax((double)(full + (rem > 0)) * per_round, t_mem);
+        // tail split: the rem rows of a last, partly idle round go to the stream kernel on the
+        // SMs no cluster can use (they run concurrently), when that finishes within the rounds
+        const int64_t idle = (int64_t)sms - (int64_t)Q * CL;
+        int64_t split = 0;
+        static const int env_split = [] {  // development: TP_CL_SPLIT=1 also splits forced sizes
+            const char* e = getenv("TP_CL_SPLIT");
+            return e ? atoi(e) : 0;
+        }();
+        if ((env_split || (!force_cl && vs_stream)) && rem > 0 && full > 0 && idle >= 8) {
+            const double t_tail = (double)rem * (double)nb / (double)idle * 4.6 + 15.0;
+            const double t_split = fmax(fmax((double)full * per_round, t_tail), t_mem);
+            if (t_split < t || env_split) t = t_split, split = rem;
+        }
+        if (best == 0 || t < best_t) {
+            best = CL, best_t = t;
+            *tail_rows = split;
+            *tail_ctas = split ? (int)idle : 0;
+        }
     }
     if (best && vs_stream) {
         const double t_st = fmax((double)rows * (double)nb / (double)sms * 4.6 + 10.0, (2.0 * in_b + out_b) / 6.0e6);
-        if (t_st < best_t) return 0;
+        if (t_st < best_t) {
+            *tail_rows = 0;
+            *tail_ctas = 0;
+            return 0;
+        }
     }
     return best;
 }
@@ -652,8 +676,8 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, SA, LA);
 }
 
-template int rowcl_choose<float>(int64_t, int64_t, int, bool);
-template int rowcl_choose<uint16_t>(int64_t, int64_t, int, bool);
+template int rowcl_choose<float>(int64_t, int64_t, int, bool, int64_t*, int*);
+template int rowcl_choose<uint16_t>(int64_t, int64_t, int, bool, int64_t*, int*);
 template cudaError_t launch_rowcl<float>(KArgs, int, const LaunchOpts&, cudaStream_t);
 template cudaError_t launch_rowcl<uint16_t>(KArgs, int, const LaunchOpts&, cudaStream_t);
 
