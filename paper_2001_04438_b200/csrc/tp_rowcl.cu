@@ -606,18 +606,26 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
         const double t_mem = (in_b + out_b + miss * in_b) / 6.0e6;
         const int64_t full = rows / Q, rem = rows - full * Q;
         double t = fmax((double)(full + (rem > 0)) * per_round, t_mem);
-        // tail split: the rem rows of a last, partly idle round go to the stream kernel on the
-        // SMs no cluster can use (they run concurrently), when that finishes within the rounds
+        // tail split: the rows of a last, partly idle round go to the stream kernel on the SMs
+        // no cluster can use, concurrently (shared DRAM counted).  Moving more rows than that to
+        // the stream launch measured no faster (C4: 1 row 368-373 us, 31 rows 372 us).
         const int64_t idle = (int64_t)sms - (int64_t)Q * CL;
         int64_t split = 0;
         static const int env_split = [] {  // development: TP_CL_SPLIT=1 also splits forced sizes
             const char* e = getenv("TP_CL_SPLIT");
             return e ? atoi(e) : 0;
         }();
-        if ((env_split || (!force_cl && vs_stream)) && rem > 0 && full > 0 && idle >= 8) {
-            const double t_tail = (double)rem * (double)nb / (double)idle * 4.6 + 15.0;
-            const double t_split = fmax(fmax((double)full * per_round, t_tail), t_mem);
-            if (t_split < t || env_split) t = t_split, split = rem;
+        if ((env_split || (!force_cl && vs_stream)) && full > 0 && idle >= 8) {
+            const double row_in = (double)nb * kBlockElems * sizeof(In), row_out = (double)nb * kBlockElems * 4.0;
+            for (int64_t F = full; F >= 1 && F >= full; --F) {
+                const int64_t T = rows - F * Q;
+                if (T <= 0 || T > 256) continue;
+                const double t_tail = (double)T * (double)nb / (double)idle * 4.6 + 15.0;
+                const double dram = ((double)(F * Q) * (row_in * (1.0 + miss) + row_out) +
+                                     (double)T * (2.0 * row_in + row_out)) / 6.0e6;
+                const double t_split = fmax(fmax((double)F * per_round, t_tail), dram);
+                if (t_split < t || (env_split && split == 0)) t = t_split, split = T;
+            }
         }
         if (best == 0 || t < best_t) {
             best = CL, best_t = t;
