@@ -408,3 +408,70 @@ def test_fresh_workspace_small_grids_repeated(algo, dtype, grid):
         assert tp.watchdog_flags(ws) == 0
     assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
     assert_parity(x, ys[0], f"{algo}/{dtype}/grid {grid}")
+
+
+def test_cuda_graph_capture_replays_bitwise():
+    # the entry points are stream-ordered, allocation-free and host-sync-free: capturable in a
+    # CUDA graph, including the cluster launch with its concurrent tail launch (fork / join events)
+    x = workloads.ragged_case(256, 16384 * 49 + 5000, -300, 300, seed=16, stream=16)
+    xd = to_dev(x)
+    y = torch.empty_like(xd)
+    ws = tp.new_workspace(*x.shape)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    tp.softmax_ex(xd, out=y, workspace=ws)
+    plan = tp.last_plan()
+    assert plan["kernel"] == "cluster" and plan["lookahead_rows"] > 0   # cluster launch + tail launch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        tp.softmax_ex(xd, out=y, workspace=ws)      # warm-up (lazy init outside the capture)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            tp.softmax_ex(xd, out=y, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        y.zero_()
+        g.replay()
+        assert np.array_equal(to_host(y), ref)
+    assert tp.watchdog_flags(ws) == 0
+
+
+def test_concurrent_streams_with_own_workspaces():
+    # two launches on two streams at once, each with its own workspace (include/twopass.h)
+    xa = to_dev(workloads.ragged_case(200, 16384 * 6 + 8, -100, 100, seed=17, stream=1))
+    xb = to_dev(workloads.ragged_case(3, 16384 * 300, -100, 100, seed=17, stream=2))
+    ra = to_host(tp.softmax_ex(xa, schedule=tp.SCHED_STREAM))
+    rb = to_host(tp.softmax_ex(xb, schedule=tp.SCHED_STREAM))
+    wa, wb = tp.new_workspace(*xa.shape), tp.new_workspace(*xb.shape)
+    ya, yb = torch.empty_like(xa), torch.empty_like(xb)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    sa.wait_stream(torch.cuda.current_stream())
+    sb.wait_stream(torch.cuda.current_stream())
+    for _ in range(3):
+        with torch.cuda.stream(sa):
+            tp.softmax_ex(xa, out=ya, workspace=wa)
+        with torch.cuda.stream(sb):
+            tp.softmax_ex(xb, out=yb, workspace=wb)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(ya), ra) and np.array_equal(to_host(yb), rb)
+    assert tp.watchdog_flags(wa) == 0 and tp.watchdog_flags(wb) == 0
+
+
+def test_workspace_reused_across_shapes_and_schedules():
+    # one workspace, alternating shapes (control regions re-zeroed on shape change) and
+    # schedules (cluster with tail split, stream, small), results stay bitwise stable
+    shapes = [(256, 16384 * 49 + 5000), (40, 16384 * 3), (256, 16384 * 49 + 5000), (7, 16384 * 2 + 40)]
+    ws = tp.new_workspace(256, 16384 * 49 + 5000)
+    refs = {}
+    for it in range(2):
+        for rows, cols in shapes:
+            x = workloads.ragged_case(rows, cols, -400, 400, seed=18, stream=rows)
+            xd = to_dev(x)
+            for sched in (tp.SCHED_AUTO, tp.SCHED_STREAM, tp.SCHED_CLUSTER):
+                y = to_host(tp.softmax_ex(xd, workspace=ws, schedule=sched))
+                assert tp.watchdog_flags(ws) == 0
+                key = (rows, cols)
+                if key not in refs:
+                    refs[key] = y
+                assert np.array_equal(y, refs[key]), (key, sched, it)
