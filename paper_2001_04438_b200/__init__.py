@@ -191,7 +191,8 @@ def partial(x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.T
     x = _prep(x)
     rows, cols = _rows_cols(x)
     p = torch.empty((rows, 2), dtype=torch.float32, device=x.device) if out is None else out
-    ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel())
+    ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(),
+                                                             workspace.numel() * workspace.element_size())
     st = lib().softmax_partial_ex(_in_dtype(x), x.data_ptr(), rows, cols, p.data_ptr(), ws_ptr, ws_bytes,
                                   _opts(grid_ctas), _stream())
     _check(st, "partial")
