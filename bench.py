@@ -285,7 +285,9 @@ def main():
         else:
             tp.softmax_ex(x, tp.ALGO_TWO_PASS, out=y, workspace=ws)
 
-    launches_per_step = 2 if (spec["mode"] == "chunk" and world > 1) else 1
+    # our kernels per step: partial + finish (+ push + wait with the NVLink exchange) for chunk
+    # shards; one launch otherwise, plus the concurrent tail launch of a split cluster launch
+    launches_per_step = (4 if args.exchange == "nvlink" else 2) if (spec["mode"] == "chunk" and world > 1) else 1
 
     def timed(step, K, W, sample_clocks=False):
         for _ in range(W):
@@ -321,6 +323,8 @@ def main():
 
     total_ms, per_launch_ms, clocks = timed(step_two_pass, args.steps, args.warmup, sample_clocks=True)
     plan = tp.last_plan()  # which kernel the timed launches ran
+    if plan["kernel"] == "cluster" and plan["lookahead_rows"] > 0:
+        launches_per_step += 1  # the tail rows' concurrent stream launch
     kernel_name = KERNEL_NAMES.get(plan["kernel"], plan["kernel"]).format(In="float" if dtype == "f32" else "uint16_t")
     if tp.watchdog_flags(ws, reset=True):
         raise RuntimeError("watchdog fired during the benchmark: results invalid")
