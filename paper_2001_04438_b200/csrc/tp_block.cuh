@@ -65,11 +65,12 @@ __device__ __forceinline__ void load_stage(const In* stage, BlockVals& r, int ti
 // From global memory.  `vec`: 16-byte aligned rows (128-bit loads); otherwise scalar loads.
 // Elements past `valid` read as 0 (callers mask).  `last` = evict-first L2 policy.
 template <typename In>
-__device__ __forceinline__ void load_global(const In* xb, int valid, bool vec, bool last, BlockVals& r) {
+__device__ __forceinline__ void load_global(const In* xb, int valid, bool vec, bool last, BlockVals& r,
+                                            int tid = (int)threadIdx.x) {
     constexpr int V = InTraits<In>::V, NV = kPerThread / V;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        const int e = vec_off<V>((int)threadIdx.x, k);
+        const int e = vec_off<V>(tid, k);
         if (vec && e + V <= valid) {
             if constexpr (V == 4) {
                 const float4* p = reinterpret_cast<const float4*>(xb + e);
