@@ -219,9 +219,30 @@ int tp_set_profile_buffer(void* device_counters);
 
 /* STREAM-style HBM baselines beside the softmax passes (measurement only):
  * what = 0 copy y = x (8 B/element), 1 scale y = a x (8), 2 in-place scale x = a x (8),
- * 3 read-only sum (4 B/element; one partial per CTA written to y[0..ctas)).  Device pointers,
+ * 3 read-only sum (4 B/element; one partial per CTA written to y[0..ctas)), 4 / 5 the read-only
+ * sum with 8 / 16 independent 128-bit loads in flight per thread (y not written).  Device pointers,
  * 16-byte aligned, n a multiple of 4; ctas = grid size (0 = 4 per SM).  Asynchronous. */
 int tp_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t stream);
+
+/* Per-pass decomposition (measurement only): runs phase `phase` (0-based; Two-Pass
+ * 0..1, Three-Pass 0..2) of `algo` alone over every block of x, on the persistent stream
+ * kernel.  A phase > 0 uses the row statistics the workspace holds from the previous FULL call
+ * of the same algo, shape and dtype with schedule TP_SCHED_STREAM on the same workspace (it
+ * does not wait for them); outputs are then those of the full call's final phase when
+ * phase = last.  Phase 0 of Two-Pass writes nothing to y (y may be NULL); the Three-Pass
+ * phases 0..1 write nothing either except Reload's phase 1 (y = exp(x - mu)).  Rows must be
+ * 16-byte aligned (cols * element size a multiple of 16, aligned base pointers), else TP_EINVAL;
+ * workspace as for softmax_ex.  Asynchronous. */
+int tp_phase_only(int algo, int in_dtype, int phase, const void* x, float* y, int64_t rows, int64_t cols,
+                  void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* HBM read-throughput probe (measurement only): the first floor(bytes / chunk_bytes) chunks of
+ * x are read with bulk (TMA) copies into shared memory, CTA c taking chunks c, c + ctas, ...
+ * through a ring of `stages` buffers of chunk_bytes (chunk_bytes a multiple of 16, stages <= 32,
+ * stages x chunk_bytes <= 227 KB).  x: device, 16-byte aligned; sink: device, ctas floats
+ * (meaningless).  Asynchronous; TP_EINVAL on bad arguments. */
+int tp_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, float* sink,
+                  cudaStream_t stream);
 
 /* Accuracy sweep hook (test/metrology only): for i < count, x = the fp32 whose
  * bit pattern is bits0 + i (the caller keeps bits0 + count - 1 <= 0xffffffff); what = 0:

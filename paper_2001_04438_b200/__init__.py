@@ -34,7 +34,7 @@ EXPORTS = [
     "softmax_bf16_partial", "softmax_f32_finish", "softmax_bf16_f32_finish", "softmax_workspace_bytes",
     "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_f32_host", "softmax_bf16_f32_host",
     "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
-    "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_exp_sweep", "tp_exp_fit",
+    "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_read_probe", "tp_phase_only", "tp_exp_sweep", "tp_exp_fit",
     "tp_mailbox_bytes", "tp_pairs_push", "tp_pairs_wait", "tp_ipc_get_handle", "tp_ipc_open", "tp_ipc_close",
 ]
 
@@ -97,6 +97,8 @@ def lib() -> ctypes.CDLL:
         L.tp_ipc_close.argtypes = [vp]
         L.tp_exp_sweep.argtypes = [ci, ctypes.c_uint32, i64, vp, vp, vp]
         L.tp_stream_baseline.argtypes = [ci, vp, vp, i64, ctypes.c_float, i64, vp]
+        L.tp_read_probe.argtypes = [vp, i64, i64, ci, i64, vp, vp]
+        L.tp_phase_only.argtypes = [ci, ci, ci, vp, vp, i64, i64, vp, ctypes.c_size_t, vp]
         L.tp_bench_compute.argtypes = [ci, ci, i64, ci, vp, vp]
         L.softmax_last_plan.argtypes = [ctypes.POINTER(SoftmaxPlan)]
         _lib = L
@@ -210,6 +212,21 @@ def finish(x: torch.Tensor, pairs: torch.Tensor, world: int, out: torch.Tensor |
     st = lib().softmax_finish_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, pairs.data_ptr(), world,
                                  _opts(grid_ctas), _stream())
     _check(st, "finish")
+    return y
+
+
+def phase_only(x: torch.Tensor, algo: int, phase: int, workspace: torch.Tensor,
+               out: torch.Tensor | None = None) -> torch.Tensor | None:
+    """Measurement hook (tp_phase_only): phase `phase` of `algo` alone; a later phase uses the
+    statistics left in `workspace` by the previous full schedule=SCHED_STREAM call."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    y = out
+    if y is None and not (algo == ALGO_TWO_PASS and phase == 0):
+        y = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    st = lib().tp_phase_only(algo, _in_dtype(x), phase, x.data_ptr(), None if y is None else y.data_ptr(), rows,
+                             cols, workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream())
+    _check(st, "phase_only")
     return y
 
 

@@ -457,7 +457,7 @@ int tp_set_profile_buffer(void* p) {
 }
 
 int tp_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t stream) {
-    if (what < 0 || what > 3 || n < 0 || (n & 3) || !x || (what != 2 && !y) ||
+    if (what < 0 || what > 5 || n < 0 || (n & 3) || !x || (what != 2 && !y) ||
         ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15))
         return TP_EINVAL;
     if (n == 0) return TP_OK;
@@ -468,6 +468,33 @@ int tp_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t
         ctas = 4 * (int64_t)sms;
     }
     cudaError_t e = tp::launch_stream_baseline(what, x, y, n, a, ctas, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int tp_phase_only(int algo, int in_dtype, int phase, const void* x, float* y, int64_t rows, int64_t cols,
+                  void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+    int st = check_args(in_dtype, x, y, rows, cols, algo != TP_ALGO_TWO_PASS || phase > 0);
+    if (st) return st;
+    if (algo != TP_ALGO_TWO_PASS && algo != TP_ALGO_THREE_PASS_RECOMPUTE && algo != TP_ALGO_THREE_PASS_RELOAD)
+        return TP_EINVAL;
+    if (!workspace || workspace_bytes < tp::workspace_bytes(rows, cols)) return TP_EINVAL;
+    if ((st = prepare_ws(workspace, rows, cols, stream))) return st;
+    cudaError_t e = tp::launch_phase_only(algo, in_dtype == TP_IN_BF16, phase, x, y, rows, cols, workspace,
+                                          tp::LaunchOpts{}, stream);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return TP_EINVAL;
+    }
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int tp_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, float* sink,
+                  cudaStream_t stream) {
+    if (!x || !sink || bytes < 0 || chunk_bytes < 16 || (chunk_bytes & 15) || stages < 1 || stages > 32 ||
+        chunk_bytes * stages > 227 * 1024 || ctas < 1 || (reinterpret_cast<uintptr_t>(x) & 15))
+        return TP_EINVAL;
+    if (bytes < chunk_bytes) return TP_OK;
+    cudaError_t e = tp::launch_read_probe(x, bytes, chunk_bytes, stages, ctas, sink, stream);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 

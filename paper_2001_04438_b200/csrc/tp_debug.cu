@@ -179,8 +179,66 @@ __global__ void __launch_bounds__(512) stream_baseline_kernel(int what, float* x
     }
 }
 
+// Read-only sum with U independent 128-bit loads in flight per thread (what 4: U = 8, 5: 16).
+template <int U>
+__global__ void __launch_bounds__(512) read_deep_kernel(const float* x, float* y, int64_t n4) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float s = 0.0f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = i + u * stride < n4 ? __ldcs(x4 + i + u * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+    }
+    if (s == 1.2345f) y[blockIdx.x] = s;  // keeps the loads alive
+}
+
+// Bulk-copy (TMA) read throughput: each CTA walks chunks blockIdx.x + k * gridDim.x of
+// chunk_bytes through a ring of `stages` shared-memory buffers, one elected thread issuing; a
+// chunk is re-issued as soon as the previous copy into its buffer has landed.
+__global__ void read_tma_kernel(const char* x, int64_t nchunks, uint32_t chunk_bytes, int stages, float* y) {
+    extern __shared__ __align__(128) unsigned char buf[];
+    __shared__ __align__(8) uint64_t bar[32];
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < stages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    int64_t c = blockIdx.x;
+    int k = 0;
+    for (; k < stages && c < nchunks; ++k, c += gridDim.x) {
+        mbar_arrive_expect_tx(&bar[k], chunk_bytes);
+        tma_load_1d_nohint(buf + (size_t)k * chunk_bytes, x + c * chunk_bytes, chunk_bytes, &bar[k]);
+    }
+    unsigned par = 0;
+    for (int64_t j = 0;; ++j) {
+        const int s = (int)(j % stages);
+        if (blockIdx.x + j * gridDim.x >= nchunks) break;
+        mbar_wait_parity(&bar[s], (par >> s) & 1u);
+        par ^= 1u << s;
+        if (c < nchunks) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bar[s], chunk_bytes);
+            tma_load_1d_nohint(buf + (size_t)s * chunk_bytes, x + c * chunk_bytes, chunk_bytes, &bar[s]);
+            c += gridDim.x;
+        }
+    }
+    if (buf[0] == 0xAB && buf[1] == 0xCD) y[blockIdx.x] = 1.0f;
+}
+
+cudaError_t launch_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, float* y,
+                              cudaStream_t s) {
+    const size_t dyn = (size_t)chunk_bytes * stages;
+    cudaFuncSetAttribute(read_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    read_tma_kernel<<<(unsigned)ctas, 32, dyn, s>>>(static_cast<const char*>(x), bytes / chunk_bytes,
+                                                   (uint32_t)chunk_bytes, stages, y);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t s) {
-    stream_baseline_kernel<<<(unsigned)ctas, 512, 0, s>>>(what, x, y, n / 4, a);
+    if (what == 4) read_deep_kernel<8><<<(unsigned)ctas, 512, 0, s>>>(x, y, n / 4);
+    else if (what == 5) read_deep_kernel<16><<<(unsigned)ctas, 512, 0, s>>>(x, y, n / 4);
+    else stream_baseline_kernel<<<(unsigned)ctas, 512, 0, s>>>(what, x, y, n / 4, a);
     return cudaGetLastError();
 }
 

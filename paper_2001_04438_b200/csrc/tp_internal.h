@@ -64,6 +64,10 @@ cudaError_t launch_finish(int in_bf16, const void* x, float* y, int64_t rows, in
 cudaError_t launch_debug(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                          cudaStream_t s);
 cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t s);
+cudaError_t launch_phase_only(int algo, int in_bf16, int phase, const void* x, float* y, int64_t rows, int64_t cols,
+                              void* ws, const LaunchOpts& o, cudaStream_t s);
+cudaError_t launch_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, float* y,
+                              cudaStream_t s);
 cudaError_t launch_exp_sweep(int what, uint32_t bits0, int64_t count, float* o0, float* o1, cudaStream_t s);
 cudaError_t launch_exp_fit(const float* c, uint32_t bits0, int64_t count, int stride, unsigned* max_bits,
                            unsigned long long* n_over2, cudaStream_t s);

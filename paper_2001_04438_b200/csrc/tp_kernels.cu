@@ -276,6 +276,41 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
     return launch_general<In, A>(a, o, s);
 }
 
+// One phase of a multi-phase algorithm on its own (measurement, tp_phase_only): the stream kernel
+// with every item in `phase`; a later phase reads the row statistics a previous full launch left
+// in the workspace instead of waiting for them.
+template <typename In, int A>
+static cudaError_t launch_phase(const void* x, float* y, int64_t rows, int64_t cols, void* ws, int phase,
+                                const LaunchOpts& o, cudaStream_t s) {
+    KArgs a{};
+    a.x = x; a.y = y; a.rows = rows; a.cols = cols;
+    a.nb = (cols + kBlockElems - 1) / kBlockElems;
+    a.ng = (a.nb + kGroupBlocks - 1) / kGroupBlocks;
+    a.total_items = rows * a.nb;
+    a.ws = static_cast<char*>(ws);
+    a.lay = ws_layout(rows, cols);
+    a.world = 1;
+    a.vec = vec_ok<In>(x, y, cols);
+    a.l2_hints = 1;
+    a.prof = profile_buffer();
+    a.phase_only = phase + 1;
+    if (!a.vec || phase < 0 || phase >= AlgoTraits<A>::P) return cudaErrorNotSupported;
+    return launch_stream<In, A>(a, o, s);
+}
+
+cudaError_t launch_phase_only(int algo, int in_bf16, int phase, const void* x, float* y, int64_t rows, int64_t cols,
+                              void* ws, const LaunchOpts& o, cudaStream_t s) {
+    switch (algo * 2 + (in_bf16 ? 1 : 0)) {
+        case kTwoPass * 2: return launch_phase<float, kTwoPass>(x, y, rows, cols, ws, phase, o, s);
+        case kTwoPass * 2 + 1: return launch_phase<uint16_t, kTwoPass>(x, y, rows, cols, ws, phase, o, s);
+        case kRecompute * 2: return launch_phase<float, kRecompute>(x, y, rows, cols, ws, phase, o, s);
+        case kRecompute * 2 + 1: return launch_phase<uint16_t, kRecompute>(x, y, rows, cols, ws, phase, o, s);
+        case kReload * 2: return launch_phase<float, kReload>(x, y, rows, cols, ws, phase, o, s);
+        case kReload * 2 + 1: return launch_phase<uint16_t, kReload>(x, y, rows, cols, ws, phase, o, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
 template <typename In>
 static cudaError_t launch_softmax_t(int algo, const void* x, float* y, int64_t rows, int64_t cols, void* ws,
                                     const LaunchOpts& o, cudaStream_t s) {

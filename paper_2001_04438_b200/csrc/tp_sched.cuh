@@ -60,6 +60,7 @@ struct KArgs {
     int vec;                 // 16-byte aligned rows
     int l2_hints;            // TMA loads carry evict_last / evict_first L2 policies
     int hold;                // stream kernel: blocks stay staged between pass 1 and pass 2
+    int phase_only;          // measurement (tp_phase_only): 1 + the one phase this launch runs, else 0
     unsigned long long* prof;  // development: per-role cycle counters (tp_set_profile_buffer), or null
 };
 

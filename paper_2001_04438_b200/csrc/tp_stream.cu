@@ -116,9 +116,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         // =============================================================== producer warp
         if (lane != 0) return;
         // development timeline (KArgs::prof): per CTA, globaltimer at start, at queue
-        // exhaustion and at exit, in prof[16 + 3 * blockIdx.x + {0, 1, 2}]
+        // exhaustion, at exit, when the first later-phase item was taken and when its row
+        // statistics were first seen, in prof[16 + 5 * blockIdx.x + {0..4}]
         const unsigned long long tl_start = a.prof ? globaltimer_ns() : 0ull;
-        unsigned long long tl_exh = 0;
+        unsigned long long tl_exh = 0, tl_p2 = 0, tl_rel = 0;
         const unsigned* row_ready = reinterpret_cast<const unsigned*>(a.ws + a.lay.row_ready);
         const In* x = static_cast<const In*>(a.x);
         const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
@@ -174,12 +175,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         // statistics of the row phase an item depends on, if released (cached per row)
         auto stats_ready = [&](const Item& it, int dep_phase, float4* st) -> bool {
             if (!(it.row == cached_row && dep_phase == cached_phase)) {
-                if (ld_acquire_gpu(row_ready + it.row * 2 + dep_phase) != want) {
+                // phase_only: the statistics are those a previous full launch left in the workspace
+                if (!a.phase_only && ld_acquire_gpu(row_ready + it.row * 2 + dep_phase) != want) {
                     const unsigned long long now = globaltimer_ns();
                     if (wait_t0 == 0) wait_t0 = now;
                     if (now - wait_t0 <= kWaitTimeoutNs) return false;
                     atomicOr(&hdr->error, 1u);  // never hang the GPU on a bug
                 }
+                if (a.prof && tl_rel == 0) tl_rel = globaltimer_ns();
                 cached_st = __ldcg(reinterpret_cast<const float4*>(a.ws + a.lay.row_stats) + it.row * 2 + dep_phase);
                 cached_row = it.row;
                 cached_phase = dep_phase;
@@ -212,11 +215,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
 
         auto issue = [&](int s, long long item) {
             Item it;
-            if (hold) {  // one item per block: (row, blk), pass 1 then pass 2 on the same stage
+            if (hold || a.phase_only) {  // one item per block: (row, blk)
                 const uint32_t u = (uint32_t)item, nb = (uint32_t)a.nb;
-                it.phase = 0;
+                it.phase = hold ? 0 : a.phase_only - 1;  // hold: pass 1 then pass 2 on the same stage
                 it.row = u / nb;
                 it.blk = u - (u / nb) * nb;
+                if (it.phase > 0) it.blk = a.nb - 1 - it.blk;
             } else {
                 it = decode_item<A>(item, a.rows, a.nb, a.L);
             }
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 mbar_arrive(&full_bar[s]);
             } else {
                 const uint32_t bytes = (uint32_t)valid * (uint32_t)sizeof(In);
-                const bool keep = !hold && ((P > 1 && it.phase < P - 1) || A == kPartial);
+                const bool keep = !hold && !a.phase_only && ((P > 1 && it.phase < P - 1) || A == kPartial);
                 In* dst = stages + (size_t)s * kBlockElems;
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(&full_bar[s], bytes);
@@ -251,6 +255,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 set_state(s, 2);  // P1 now, P2 once the row is released
                 push(kOpP1, s, parity);
             } else if (item_needs_stats<A>(it) && A != kFinish) {
+                if (a.prof && tl_p2 == 0) tl_p2 = globaltimer_ns();
                 set_state(s, 2);
                 poll();
             } else {
@@ -289,9 +294,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         push(kOpExit, 0, 0);
         if (!hold && ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
         if (a.prof) {
-            a.prof[16 + 3 * blockIdx.x] = tl_start;
-            a.prof[16 + 3 * blockIdx.x + 1] = tl_exh;
-            a.prof[16 + 3 * blockIdx.x + 2] = globaltimer_ns();
+            unsigned long long* t = a.prof + 16 + 5 * blockIdx.x;
+            t[0] = tl_start;
+            t[1] = tl_exh;
+            t[2] = globaltimer_ns();
+            t[3] = tl_p2;
+            t[4] = tl_rel;
         }
         exit_and_reset(hdr);
     } else if (warp == kRetireWarp) {
@@ -330,9 +338,24 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
     } else {
         // =============================================================== compute warps
         long long pseq = 0;  // part slots used
+        // development (KArgs::prof): compute warp cycle accounting, summed over CTAs into
+        // prof[0..7] = command wait, data wait, part-slot wait, pass-1 ops, later-phase ops,
+        // total, pass-1 blocks, later-phase blocks (warp 0 of each CTA)
+        const bool pc_on = a.prof != nullptr && warp == 0;
+        unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const unsigned long long pc_start = pc_on ? clock64() : 0ull;
+        unsigned long long pt = pc_start;
+        auto lap = [&](int slot) {
+            if (pc_on) {
+                const unsigned long long now = clock64();
+                pc[slot] += now - pt;
+                pt = now;
+            }
+        };
         for (long long c = 0;; ++c) {
             const int cs = (int)(c % C);
             if (!wait_or_abort(&cfull_bar[cs], (uint32_t)((c / C) & 1), &hdr->error, 8u)) break;
+            lap(0);
             const Cmd cmd = cmds[cs];
             __syncwarp();
             if (lane == 0) mbar_arrive(&cempty_bar[cs]);
@@ -352,6 +375,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             const int r = (int)(pseq % R);
             if (pseq >= R && !wait_or_abort(&pempty_bar[r], (uint32_t)(((pseq / R) - 1) & 1), &hdr->error, 16u)) break;
             ++pseq;
+            lap(2);
             PartSlot& ps = pslot[r];
             if (cmd.op == kOpExit) {  // pass the end on to the retire warp
                 if (warp == 0 && lane == 0) ps.item = total;
@@ -360,6 +384,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 break;
             }
             if (!wait_or_abort(&full_bar[s], cmd.parity, &hdr->error, 4u)) break;
+            lap(1);
             const long long item = meta[s].item;  // read everything before the stage is released
             const Item it = meta[s].it;
             const int valid = meta[s].valid;
@@ -395,6 +420,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&pfull_bar[r]);
+            if (pc_on) {
+                lap(it.phase == 0 ? 3 : 4);
+                ++pc[it.phase == 0 ? 6 : 7];
+            }
+        }
+        if (pc_on && lane == 0) {
+            pc[5] = clock64() - pc_start;
+            for (int i = 0; i < 8; ++i) atomicAdd(&a.prof[i], pc[i]);
         }
     }
 }
@@ -415,8 +448,8 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     int64_t grid = o.grid_ctas > 0 ? o.grid_ctas : resident;
     if (grid > resident) grid = resident;
     // hold mode: Two-Pass rows of several blocks that fit the grid's stages four times over
-    a.hold = (A == kTwoPass && o.schedule == 2 && a.nb >= 2 && a.nb * 4 <= grid * S) ? 1 : 0;
-    if (a.hold) a.total_items = a.rows * a.nb;
+    a.hold = (A == kTwoPass && o.schedule == 2 && a.nb >= 2 && a.nb * 4 <= grid * S && !a.phase_only) ? 1 : 0;
+    if (a.hold || a.phase_only) a.total_items = a.rows * a.nb;
     if (grid > a.total_items) grid = a.total_items;
     if (grid < 1) grid = 1;
     // stream mode: items a CTA holds between hand-out and retirement (its stages, the prefetched

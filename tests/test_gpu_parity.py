@@ -475,3 +475,44 @@ def test_workspace_reused_across_shapes_and_schedules():
                 if key not in refs:
                     refs[key] = y
                 assert np.array_equal(y, refs[key]), (key, sched, it)
+
+
+# ------------------------------------------------------------------ per-pass measurement hook
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", [(5, 16384 * 6 + 1000), (1, 1 << 20)])
+def test_phase_only_reproduces_the_full_call(shape, dtype):
+    # tp_phase_only (tools/pass_decomp.py): each pass alone on the stream kernel; the last pass,
+    # fed the statistics of a full stream-schedule call, reproduces that call bit for bit
+    x = workloads.ragged_case(*shape, -300, 300, seed=17, stream=shape[0])
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    for algo in ("two_pass", "recompute"):
+        a = ALGOS[algo]
+        ws = tp.new_workspace(*x.shape)
+        full = to_host(tp.softmax_ex(xd, a, workspace=ws, schedule=tp.SCHED_STREAM))
+        for ph in range(2 if algo == "two_pass" else 3):
+            y = tp.phase_only(xd, a, ph, ws)
+            assert tp.watchdog_flags(ws) == 0
+        assert np.array_equal(to_host(y), full), algo
+    # Reload: pass 2 alone writes exp(x - mu) into y, pass 3 alone scales it in place
+    ws = tp.new_workspace(*x.shape)
+    full = to_host(tp.softmax_ex(xd, tp.ALGO_RELOAD, workspace=ws, schedule=tp.SCHED_STREAM))
+    tp.phase_only(xd, tp.ALGO_RELOAD, 0, ws)
+    y = tp.phase_only(xd, tp.ALGO_RELOAD, 1, ws)
+    tp.phase_only(xd, tp.ALGO_RELOAD, 2, ws, out=y)
+    assert tp.watchdog_flags(ws) == 0
+    assert np.array_equal(to_host(y), full)
+    assert_parity(x, full, f"reload/{dtype}")
+
+
+def test_phase_only_rejects_bad_arguments():
+    xd = to_dev(workloads.ragged_case(2, 16384 * 3, seed=18))
+    ws = tp.new_workspace(*xd.shape)
+    for algo, ph in ((tp.ALGO_TWO_PASS, 2), (tp.ALGO_RECOMPUTE, 3), (tp.ALGO_TWO_PASS, -1), (1, 0)):
+        with pytest.raises(tp.TwoPassError):
+            tp.phase_only(xd, algo, ph, ws, out=torch.empty_like(xd))
+    with pytest.raises(tp.TwoPassError):  # misaligned rows: the stream kernel only
+        xm = to_dev(workloads.ragged_case(2, 16384 + 3, seed=18))
+        tp.phase_only(xm, tp.ALGO_TWO_PASS, 0, tp.new_workspace(*xm.shape))

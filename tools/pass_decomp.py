@@ -6,8 +6,11 @@
 For each workload (fp32): STREAM copy / scale / in-place scale / read-only sum over the same
 number of elements, Two-Pass pass 1 alone (softmax_partial_ex: read x, one (m, n) per row),
 pass 2 alone (softmax_finish_ex with those pairs: read x, write y), the whole Two-Pass on the
-default and on the stream schedule, and the Three-Pass comparators.  Every rep is preceded by
-an L2 flush (512 MB write) and timed with CUDA events on the launching stream; medians.
+default and on the stream schedule, the Three-Pass comparators, and every pass of every
+algorithm alone on the stream kernel (tp_phase_only: the paper's per-pass runtime figure,
+PAPER.md:323-329).  Every rep is preceded by
+an L2 flush (512 MB write, then a 512 MB read so that no dirty line is left to write back
+inside the timed region) and timed with CUDA events on the launching stream; medians.
 GB/s use each kernel's own compulsory bytes (Table 2 l.180-198).
 """
 import argparse
@@ -23,12 +26,21 @@ import paper_2001_04438_b200 as tp  # noqa: E402
 import workloads  # noqa: E402
 
 
+def clean_flush(flush):
+    """Evict L2 and leave it holding CLEAN lines: a 512 MB write alone would leave ~126 MB of
+    dirty lines whose write-back then lands inside the timed kernel."""
+    flush.zero_()
+    f = flush.view(torch.float32)
+    tp.lib().tp_stream_baseline(4, f.data_ptr(), f.data_ptr(), f.numel(), 1.0, 0,
+                                torch.cuda.current_stream().cuda_stream)
+
+
 def timeit(fn, reps, flush):
     for _ in range(3):
         fn()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        clean_flush(flush)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
@@ -71,15 +83,28 @@ def main():
             ("three_pass_recompute", lambda: tp.softmax_ex(x, tp.ALGO_RECOMPUTE, out=y, workspace=ws), 16),
             ("three_pass_reload", lambda: tp.softmax_ex(x, tp.ALGO_RELOAD, out=y, workspace=ws), 20),
         ]
+        # each pass of each algorithm alone (tp_phase_only, stream kernel; the statistics of the
+        # later passes come from a full stream-schedule call on the same workspace first):
+        # the paper's Fig. "absolute runtime of the passes"
+        pws = {a: tp.new_workspace(rows, cols) for a in (tp.ALGO_TWO_PASS, tp.ALGO_RECOMPUTE, tp.ALGO_RELOAD)}
+        ybuf = torch.empty_like(x)
+        for a, pws_a in pws.items():
+            tp.softmax_ex(x, a, out=ybuf, workspace=pws_a, schedule=tp.SCHED_STREAM)
+        phase_bytes = {("two_pass", 0): 4, ("two_pass", 1): 8, ("recompute", 0): 4, ("recompute", 1): 4,
+                       ("recompute", 2): 8, ("reload", 0): 4, ("reload", 1): 8, ("reload", 2): 8}
+        anum = {"two_pass": tp.ALGO_TWO_PASS, "recompute": tp.ALGO_RECOMPUTE, "reload": tp.ALGO_RELOAD}
+        for (an, ph), bpe in phase_bytes.items():
+            cases.append((f"{an}_phase{ph + 1}_alone",
+                          (lambda an=an, ph=ph: tp.phase_only(x, anum[an], ph, pws[anum[an]], out=ybuf)), bpe))
         for name, fn, bpe in cases:
             t = timeit(fn, args.reps, flush)
             rec = {"config": key, "kernel": name, "median_us": round(t * 1e6, 2), "bytes_per_elem": bpe,
                    "GBps": round(bpe * n / t / 1e9, 1), "elems_per_s": n / t}
-            if name.startswith("two_pass") or name.startswith("three"):
+            if name.startswith(("two_pass", "three", "recompute", "reload")):
                 rec["plan"] = tp.last_plan()
             out.append(rec)
             print(json.dumps(rec), flush=True)
-        del x, y, tmp, ws
+        del x, y, tmp, ws, pws, ybuf
         torch.cuda.empty_cache()
     assert tp.watchdog_flags() == 0
     if args.json:
