@@ -230,7 +230,7 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-three-pass", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "nvlink"],
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "nvlink", "nvlink-fused"],
                     help="rank merge of chunk-sharded rows: NCCL all_gather or one-sided NVLink mailboxes")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -276,17 +276,17 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     peer = None
-    if spec["mode"] == "chunk" and world > 1 and args.exchange == "nvlink":
+    if spec["mode"] == "chunk" and world > 1 and args.exchange.startswith("nvlink"):
         peer = tpd.PeerPairExchange(rows, dev)
 
     def step_two_pass():
         if spec["mode"] == "chunk" and world > 1:
-            tpd.chunk_sharded_softmax(x, out=y, workspace=ws, exchange=peer)
+            tpd.chunk_sharded_softmax(x, out=y, workspace=ws, exchange=peer, fused=args.exchange == "nvlink-fused")
         else:
             tp.softmax_ex(x, tp.ALGO_TWO_PASS, out=y, workspace=ws)
 
-    # our kernels per step: partial + finish (+ push + wait with the NVLink exchange) for chunk
-    # shards; one launch otherwise, plus the concurrent tail launch of a split cluster launch
+    # our kernels per step: partial + finish (+ push + wait with the unfused NVLink exchange) for
+    # chunk shards; one launch otherwise, plus the concurrent tail launch of a split cluster launch
     launches_per_step = (4 if args.exchange == "nvlink" else 2) if (spec["mode"] == "chunk" and world > 1) else 1
 
     def timed(step, K, W, sample_clocks=False):
@@ -389,8 +389,10 @@ def main():
                              (n_local * (4 if dtype == 'f32' else 2) / 1e6),
                        "parallelism": ("rows sharded, no collective" if spec["mode"] == "rows" else
                                        "row chunk-sharded, one 8-byte (m,n) per rank exchanged by " +
-                                       ("one-sided NVLink mailboxes" if args.exchange == "nvlink" else
-                                        "NCCL all_gather"))},
+                                       ({"nvlink": "one-sided NVLink mailboxes (push / wait kernels)",
+                                         "nvlink-fused": "one-sided NVLink mailboxes, pushed by the pass-1 kernel "
+                                                         "and awaited by the pass-2 kernel"}.get(args.exchange,
+                                                                                              "NCCL all_gather")))},
             "elements_per_s": elems_total / (ms_per_step * 1e-3),
             "pct_of_8TBs": value / world / NOMINAL_HBM_GBS if spec["scaling"] == "weak" else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

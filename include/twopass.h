@@ -159,6 +159,29 @@ int softmax_partial_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, 
 int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
                       int world, const softmax_opts* opts, cudaStream_t stream);
 
+/* ---- fused one-sided exchange (pass 1 + rank merge a7 without a collective
+ * library or extra launches; mailboxes as for tp_pairs_push / tp_pairs_wait above) ----------
+ * softmax_partial_push_ex: pass 1 of Alg. 3 over this rank's chunk of each
+ *   row, as softmax_partial_ex; inside the same kernel, the thread that finishes a row's
+ *   pair stores it into slot `rank` of every mailbox in peer_mailboxes (DEVICE array of world
+ *   pointers, as tp_pairs_push) and, once all `rows` pairs are stored and fenced system-wide,
+ *   release-stores `epoch` (>= 1, new per exchange) into flag `rank` of every mailbox.
+ *   pair_out (device, rows x 2) also receives the pairs when not NULL.
+ * softmax_finish_mailbox_ex: as softmax_finish_ex with pairs = mailbox + 256 bytes, except
+ *   that the kernel itself first waits (acquire, system scope) until the world flags of the
+ *   LOCAL mailbox equal `epoch`; a flag missing for timeout_ns sets its rank's bit in the
+ *   mailbox error word and watchdog bit 0 (outputs then undefined; nothing hangs).
+ * Sequence per rank: partial_push -> finish_mailbox, two launches, no NCCL, no host
+ * synchronisation.  Results are bit-identical to partial -> all_gather -> finish.
+ * TP_EINVAL: bad sizes / pointers, world outside 1..56, rank outside [0, world), epoch 0,
+ * mailbox not 16-byte aligned.  Asynchronous. */
+int softmax_partial_push_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, void* const* peer_mailboxes,
+                            int rank, int world, unsigned epoch, float* pair_out, void* workspace,
+                            size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream);
+int softmax_finish_mailbox_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const void* mailbox,
+                              int world, unsigned epoch, unsigned long long timeout_ns, const softmax_opts* opts,
+                              cudaStream_t stream);
+
 /* ---- end-to-end call on HOST buffers ---------------------------------------
  * hx, hy: HOST pointers (pinned memory gives full PCIe bandwidth).  Copies x to
  * the current device, runs softmax_f32 / softmax_bf16_f32, copies y back and

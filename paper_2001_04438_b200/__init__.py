@@ -32,7 +32,7 @@ EXPORTS = [
     "softmax_f32", "softmax_bf16_f32", "softmax3_recompute_f32", "softmax3_reload_f32",
     "softmax3_recompute_bf16_f32", "softmax3_reload_bf16_f32", "softmax_f32_partial",
     "softmax_bf16_partial", "softmax_f32_finish", "softmax_bf16_f32_finish", "softmax_workspace_bytes",
-    "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_f32_host", "softmax_bf16_f32_host",
+    "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_partial_push_ex", "softmax_finish_mailbox_ex", "softmax_f32_host", "softmax_bf16_f32_host",
     "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
     "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_read_probe", "tp_phase_only", "tp_exp_sweep", "tp_exp_fit",
     "tp_mailbox_bytes", "tp_pairs_push", "tp_pairs_wait", "tp_ipc_get_handle", "tp_ipc_open", "tp_ipc_close",
@@ -80,6 +80,10 @@ def lib() -> ctypes.CDLL:
         L.softmax_ex.argtypes = [ci, ci, vp, vp, i64, i64, vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
         L.softmax_partial_ex.argtypes = [ci, vp, i64, i64, vp, vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
         L.softmax_finish_ex.argtypes = [ci, vp, vp, i64, i64, vp, ci, ctypes.POINTER(SoftmaxOpts), vp]
+        L.softmax_partial_push_ex.argtypes = [ci, vp, i64, i64, vp, ci, ci, ctypes.c_uint, vp, vp, sz,
+                                              ctypes.POINTER(SoftmaxOpts), vp]
+        L.softmax_finish_mailbox_ex.argtypes = [ci, vp, vp, i64, i64, vp, ci, ctypes.c_uint, ctypes.c_ulonglong,
+                                                ctypes.POINTER(SoftmaxOpts), vp]
         L.softmax_f32_host.argtypes = [vp, vp, i64, i64]
         L.softmax_bf16_f32_host.argtypes = [vp, vp, i64, i64]
         L.softmax_status_str.argtypes = [ci]
@@ -212,6 +216,35 @@ def finish(x: torch.Tensor, pairs: torch.Tensor, world: int, out: torch.Tensor |
     st = lib().softmax_finish_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, pairs.data_ptr(), world,
                                  _opts(grid_ctas), _stream())
     _check(st, "finish")
+    return y
+
+
+def partial_push(x: torch.Tensor, peer_ptrs: torch.Tensor, rank: int, world: int, epoch: int,
+                 pair_out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                 grid_ctas: int = 0) -> None:
+    """Pass 1 over a chunk of each row; the kernel pushes the row pairs into slot `rank` of every
+    mailbox (peer_ptrs: device int64 [world]) and releases `epoch` (softmax_partial_push_ex)."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    assert peer_ptrs.is_cuda and peer_ptrs.dtype == torch.int64 and peer_ptrs.numel() == world
+    ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(),
+                                                             workspace.numel() * workspace.element_size())
+    st = lib().softmax_partial_push_ex(_in_dtype(x), x.data_ptr(), rows, cols, peer_ptrs.data_ptr(), rank, world,
+                                       epoch, None if pair_out is None else pair_out.data_ptr(), ws_ptr, ws_bytes,
+                                       _opts(grid_ctas), _stream())
+    _check(st, "partial_push")
+
+
+def finish_mailbox(x: torch.Tensor, mailbox: torch.Tensor, world: int, epoch: int, timeout_ns: int,
+                   out: torch.Tensor | None = None, grid_ctas: int = 0) -> torch.Tensor:
+    """Await `epoch` in the local mailbox inside the kernel, merge its world pairs per row, pass 2
+    (softmax_finish_mailbox_ex)."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
+    st = lib().softmax_finish_mailbox_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, mailbox.data_ptr(),
+                                         world, epoch, timeout_ns, _opts(grid_ctas), _stream())
+    _check(st, "finish_mailbox")
     return y
 
 

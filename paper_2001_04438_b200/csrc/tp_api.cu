@@ -393,6 +393,52 @@ int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64
                       int world, const softmax_opts* opts, cudaStream_t stream) {
     return run_finish(in_dtype, x, y, rows, cols, pairs, world, opts, stream);
 }
+int softmax_partial_push_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, void* const* peer_mailboxes,
+                            int rank, int world, unsigned epoch, float* pair_out, void* workspace,
+                            size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream) {
+    int st = check_args(in_dtype, x, nullptr, rows, cols, false);
+    if (st) return st;
+    if (!peer_mailboxes || world < 1 || world > tp::kMailboxMaxWorld || rank < 0 || rank >= world || epoch == 0)
+        return TP_EINVAL;
+    void* ws = workspace;
+    const size_t need = tp::workspace_bytes(rows, cols);
+    if (ws) {
+        if (workspace_bytes < need) return TP_EINVAL;
+    } else if ((st = internal_workspace(need, &ws))) {
+        return st;
+    }
+    if ((st = prepare_ws(ws, rows, cols, stream))) return st;
+    tp::Exchange xc;
+    xc.peers = peer_mailboxes;
+    xc.rank = rank;
+    xc.world = world;
+    xc.epoch = epoch;
+    cudaError_t e = tp::launch_partial(in_dtype == TP_IN_BF16, x, rows, cols, pair_out, ws, to_opts(opts), stream, &xc);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int softmax_finish_mailbox_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const void* mailbox,
+                              int world, unsigned epoch, unsigned long long timeout_ns, const softmax_opts* opts,
+                              cudaStream_t stream) {
+    int st = check_args(in_dtype, x, y, rows, cols, true);
+    if (st) return st;
+    if (!mailbox || world < 1 || world > tp::kMailboxMaxWorld || epoch == 0 ||
+        (reinterpret_cast<uintptr_t>(mailbox) & 15))
+        return TP_EINVAL;
+    void* ws = nullptr;
+    if ((st = internal_workspace(tp::workspace_bytes(rows, cols), &ws))) return st;
+    if ((st = prepare_ws(ws, rows, cols, stream))) return st;
+    tp::Exchange xc;
+    xc.world = world;
+    xc.epoch = epoch;
+    xc.mailbox = mailbox;
+    xc.wait_ns = timeout_ns;
+    const float* pairs = reinterpret_cast<const float*>(static_cast<const char*>(mailbox) + tp::kMailboxHeader);
+    cudaError_t e = tp::launch_finish(in_dtype == TP_IN_BF16, x, y, rows, cols, pairs, world, ws, to_opts(opts),
+                                      stream, &xc);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
 int softmax_f32_host(const float* hx, float* hy, int64_t rows, int64_t cols) {
     return host_pipeline(TP_IN_F32, hx, hy, rows, cols);
 }
@@ -516,7 +562,7 @@ int tp_exp_fit(const float* coeffs, uint32_t bits0, int64_t count, int stride, u
 }
 
 size_t tp_mailbox_bytes(int world, int64_t rows) {
-    return (world < 1 || world > 56 || rows < 0) ? 0 : tp::mailbox_bytes(world, rows);
+    return (world < 1 || world > tp::kMailboxMaxWorld || rows < 0) ? 0 : tp::mailbox_bytes(world, rows);
 }
 
 int tp_pairs_push(const float* pairs, int64_t rows, void* const* peer_mailboxes, int rank, int world,

@@ -535,4 +535,14 @@ __device__ __forceinline__ void tma_load_1d_nohint(void* smem_dst, const void* g
                  : "memory");
 }
 
+// System-scope release store / acquire load (flags read by peer GPUs over NVLink).
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 }  // namespace tp

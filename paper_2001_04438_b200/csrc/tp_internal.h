@@ -13,7 +13,14 @@ struct WsHeader {
     unsigned exit_ticket;        // CTAs that left the kernel
     unsigned epoch;              // launches completed; row flags are valid when == epoch + 1
     unsigned error;              // watchdog: bit 0 = a wait for a row flag timed out
+    unsigned rows_done;          // kPartial with a fused push: rows whose pair has been pushed
 };
+
+// Mailbox of the one-sided pair exchange: uint32 flags[world] at 0, error word at byte 240, then
+// float2 pairs[world][rows] (rank-major, the layout kFinish's pairs_in reads).
+constexpr size_t kMailboxHeader = 256;
+constexpr size_t kMailboxErrorWord = 240;
+constexpr int kMailboxMaxWorld = 56;
 
 constexpr unsigned long long kWaitTimeoutNs = 4000000000ull;  // 4 s: only a bug can wait this long
 
@@ -55,10 +62,20 @@ size_t tail_ctrl_bytes(int64_t rows, int64_t cols);
 bool softmax_needs_workspace(int algo, int64_t cols, const LaunchOpts& o);
 cudaError_t launch_softmax(int algo, int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, void* ws,
                            const LaunchOpts& o, cudaStream_t s);
+// Fused one-sided exchange (tp_ops.cuh push_row_pair / finish_wait): the partial launch pushes
+// its row pairs into every mailbox and releases `epoch`; the finish launch awaits the epoch in
+// the local mailbox and reads the pairs from it.
+struct Exchange {
+    void* const* peers = nullptr;  // device array of world mailbox pointers (partial)
+    int rank = 0, world = 1;
+    unsigned epoch = 0;
+    const void* mailbox = nullptr;  // local mailbox (finish)
+    unsigned long long wait_ns = 0;
+};
 cudaError_t launch_partial(int in_bf16, const void* x, int64_t rows, int64_t cols, float* pair_out, void* ws,
-                           const LaunchOpts& o, cudaStream_t s);
+                           const LaunchOpts& o, cudaStream_t s, const Exchange* xc = nullptr);
 cudaError_t launch_finish(int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
-                          int world, void* ws, const LaunchOpts& o, cudaStream_t s);
+                          int world, void* ws, const LaunchOpts& o, cudaStream_t s, const Exchange* xc = nullptr);
 
 // debug / unit-test kernels (tp_debug.cu)
 cudaError_t launch_debug(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,

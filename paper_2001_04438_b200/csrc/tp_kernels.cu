@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kThreads, 1) general_kernel(const KArgs a) {
         if (item < a.total_items) s_dec[b] = decode_item<A>(item, a.rows, a.nb, a.L);
     };
     if (threadIdx.x == 0) {
+        if (A == kFinish && a.mailbox) finish_wait(a);  // fused NVLink exchange: the peers' pairs
         s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
         s_cur_row = -1;
         fetch(0);
@@ -237,8 +238,16 @@ static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_c
 
 template <typename In, int A>
 static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t cols, void* ws, float2* pair_out,
-                               const float2* pairs_in, int world, const LaunchOpts& o, cudaStream_t s) {
+                               const float2* pairs_in, int world, const LaunchOpts& o, cudaStream_t s,
+                               const Exchange* xc = nullptr) {
     KArgs a{};
+    if (xc) {
+        a.peers = reinterpret_cast<char* const*>(xc->peers);
+        a.rank = xc->rank;
+        a.xepoch = xc->epoch;
+        a.mailbox = static_cast<const char*>(xc->mailbox);
+        a.wait_ns = xc->wait_ns;
+    }
     a.x = x; a.y = y; a.rows = rows; a.cols = cols;
     a.nb = (cols + kBlockElems - 1) / kBlockElems;
     a.ng = (a.nb + kGroupBlocks - 1) / kGroupBlocks;
@@ -334,17 +343,18 @@ cudaError_t launch_softmax(int algo, int in_bf16, const void* x, float* y, int64
 bool softmax_needs_workspace(int, int64_t, const LaunchOpts&) { return true; }
 
 cudaError_t launch_partial(int in_bf16, const void* x, int64_t rows, int64_t cols, float* pair_out, void* ws,
-                           const LaunchOpts& o, cudaStream_t s) {
+                           const LaunchOpts& o, cudaStream_t s, const Exchange* xc) {
     float2* po = reinterpret_cast<float2*>(pair_out);
-    return in_bf16 ? launch_algo<uint16_t, kPartial>(x, nullptr, rows, cols, ws, po, nullptr, 1, o, s)
-                   : launch_algo<float, kPartial>(x, nullptr, rows, cols, ws, po, nullptr, 1, o, s);
+    const int world = xc ? xc->world : 1;
+    return in_bf16 ? launch_algo<uint16_t, kPartial>(x, nullptr, rows, cols, ws, po, nullptr, world, o, s, xc)
+                   : launch_algo<float, kPartial>(x, nullptr, rows, cols, ws, po, nullptr, world, o, s, xc);
 }
 
 cudaError_t launch_finish(int in_bf16, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
-                          int world, void* ws, const LaunchOpts& o, cudaStream_t s) {
+                          int world, void* ws, const LaunchOpts& o, cudaStream_t s, const Exchange* xc) {
     const float2* pi = reinterpret_cast<const float2*>(pairs);
-    return in_bf16 ? launch_algo<uint16_t, kFinish>(x, y, rows, cols, ws, nullptr, pi, world, o, s)
-                   : launch_algo<float, kFinish>(x, y, rows, cols, ws, nullptr, pi, world, o, s);
+    return in_bf16 ? launch_algo<uint16_t, kFinish>(x, y, rows, cols, ws, nullptr, pi, world, o, s, xc)
+                   : launch_algo<float, kFinish>(x, y, rows, cols, ws, nullptr, pi, world, o, s, xc);
 }
 
 }  // namespace tp

@@ -108,6 +108,43 @@ __device__ __forceinline__ float2 block_value(const KArgs& a, const Item& it, co
     return make_float2(block_tree_warps_sum(s), 0.0f);
 }
 
+// Fused one-sided exchange, push side (one thread, when a row's pass-1 pair is final): store
+// the pair into slot `rank` of every mailbox (P2P stores over NVLink), make it visible
+// system-wide, count the row; the thread that completes the launch's last row releases the
+// exchange epoch into flag `rank` of every mailbox (after its own system fence, so every row's
+// stores, each fenced before its count, precede the flag).  The count returns to 0 for the next
+// launch.
+__device__ __forceinline__ void push_row_pair(const KArgs& a, int64_t row, float2 root) {
+    for (int p = 0; p < a.world; ++p)
+        reinterpret_cast<float2*>(a.peers[p] + kMailboxHeader)[(int64_t)a.rank * a.rows + row] = root;
+    __threadfence_system();
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
+    if (atomicAdd(&hdr->rows_done, 1u) == (unsigned)(a.rows - 1)) {
+        hdr->rows_done = 0u;
+        __threadfence_system();
+        for (int p = 0; p < a.world; ++p) st_release_sys(reinterpret_cast<unsigned*>(a.peers[p]) + a.rank, a.xepoch);
+    }
+}
+
+// Fused one-sided exchange, wait side (one thread per CTA, before its first kFinish item):
+// acquire the world flags of the local mailbox for this epoch.  A peer missing for wait_ns sets
+// its bit in the mailbox error word and watchdog bit 0 (the launch then runs on whatever pairs
+// are there, as after the separate wait kernel; the host reads the flags).
+__device__ __forceinline__ void finish_wait(const KArgs& a) {
+    const unsigned long long t0 = globaltimer_ns();
+    for (int p = 0; p < a.world; ++p) {
+        const unsigned* flag = reinterpret_cast<const unsigned*>(a.mailbox) + p;
+        while (ld_acquire_sys(flag) != a.xepoch) {
+            if (globaltimer_ns() - t0 > a.wait_ns) {
+                atomicOr(reinterpret_cast<unsigned*>(const_cast<char*>(a.mailbox) + kMailboxErrorWord), 1u << (p & 31));
+                atomicOr(&reinterpret_cast<WsHeader*>(a.ws)->error, 1u);
+                break;
+            }
+            __nanosleep(128);
+        }
+    }
+}
+
 // Publish a batch of block values (one whole warp; each lane with `mine` holds one item's
 // value): every lane stores its value, ONE fence covers the batch, every lane takes its group
 // ticket; then each group completed by the batch is reduced by the warp (canonical tree), and
@@ -161,7 +198,8 @@ __device__ void retire_batch(const KArgs& a, bool mine, const Item& it, float2 v
                 row_clamp[row] = 0u;
             }
             if (A == kPartial) {
-                a.pair_out[row] = root;
+                if (a.pair_out) a.pair_out[row] = root;
+                if (a.peers) push_row_pair(a, row, root);
             } else {
                 float4 st = row_stats_of<A>(phase, root, mu_l);
                 if (A == kTwoPass) st.z = clamped;

@@ -11,22 +11,10 @@
 // Flags are epoch-tagged, so mailboxes are never reset between calls.
 #include <cstdint>
 
-#include "tp_common.cuh"
-#include "tp_internal.h"
+#include "tp_sched.cuh"
 
 namespace tp {
 
-constexpr size_t kMailboxHeader = 256;  // flags[world] (uint32), error word at byte 240
-constexpr int kMailboxMaxWorld = 56;
-
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 __global__ void pairs_push_kernel(const float2* pairs, int64_t rows, char* const* mailboxes, int rank, int world,
                                   unsigned epoch) {
@@ -46,7 +34,7 @@ __global__ void pairs_wait_kernel(const char* mailbox, int world, unsigned epoch
     const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_sys(flag) != epoch) {
         if (globaltimer_ns() - t0 > timeout_ns) {  // never hang the GPU on a missing peer
-            atomicOr(reinterpret_cast<unsigned*>(const_cast<char*>(mailbox) + 240), 1u << (threadIdx.x & 31));
+            atomicOr(reinterpret_cast<unsigned*>(const_cast<char*>(mailbox) + kMailboxErrorWord), 1u << (threadIdx.x & 31));
             return;
         }
         __nanosleep(64);

@@ -61,6 +61,12 @@ struct KArgs {
     int l2_hints;            // TMA loads carry evict_last / evict_first L2 policies
     int hold;                // stream kernel: blocks stay staged between pass 1 and pass 2
     int phase_only;          // measurement (tp_phase_only): 1 + the one phase this launch runs, else 0
+    // fused one-sided NVLink exchange (tp_peer.cu mailbox layout):
+    char* const* peers;      // kPartial: world mailboxes (device array) the row pairs are pushed to, or null
+    int rank;                // kPartial: this rank's slot in every mailbox
+    unsigned xepoch;         // exchange epoch released into flag `rank` (kPartial) / awaited (kFinish)
+    const char* mailbox;     // kFinish: the local mailbox whose flags are awaited in-kernel, or null
+    unsigned long long wait_ns;  // kFinish: give up (error bits) after this long
     unsigned long long* prof;  // development: per-role cycle counters (tp_set_profile_buffer), or null
 };
 

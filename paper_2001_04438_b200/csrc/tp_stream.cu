@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             }
         };
 
+        if (A == kFinish && a.mailbox) finish_wait(a);  // fused NVLink exchange: the peers' pairs
         for (;;) {
             if (aborted(&hdr->error)) return;  // watchdog: every role leaves
             poll();

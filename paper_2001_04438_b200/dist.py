@@ -14,7 +14,9 @@ One process per GPU, torch.distributed for the plumbing.
   * One-sided alternative: `PeerPairExchange` gives every rank a mailbox in
     its own HBM, maps the peers' mailboxes through CUDA IPC once, and exchanges the pairs with
     the library's push kernel (P2P stores over NVLink + release flags) and wait kernel
-    (acquire flags): no NCCL launch per call, no host synchronisation.
+    (acquire flags): no NCCL launch per call, no host synchronisation.  Fused form: the
+    partial kernel pushes each row's pair as it finishes it and releases the flag after the
+    last row; the finish kernel acquires the flags itself: two launches per call in all.
 
 The kernels are the library's (partial / finish / push / wait through the C ABI); this module
 only partitions and exchanges handles.
@@ -133,6 +135,26 @@ class PeerPairExchange:
         self.push(local_pairs, self.epoch)
         return self.wait(self.epoch)
 
+    # fused path: pass 1 pushes its pairs from inside the partial kernel and the finish kernel
+    # awaits them itself (softmax_partial_push_ex / softmax_finish_mailbox_ex): two launches
+
+    def push_partial(self, x_chunk: torch.Tensor, workspace: torch.Tensor | None = None) -> int:
+        """Pass 1 of this rank's chunk with the in-kernel push; returns the epoch to finish with."""
+        self.epoch += 1
+        if x_chunk.shape[-1] == 0:  # an empty trailing chunk contributes the identity (0, -inf)
+            ident = torch.tensor([[0.0, float("-inf")]] * self.rows, dtype=torch.float32, device=x_chunk.device)
+            self.push(ident, self.epoch)
+        else:
+            self.tp.partial_push(x_chunk, self.peer_ptrs, self.rank, self.world, self.epoch, workspace=workspace)
+        return self.epoch
+
+    def finish(self, x_chunk: torch.Tensor, epoch: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Await `epoch` in the local mailbox inside the finish kernel, merge, pass 2."""
+        if x_chunk.shape[-1] == 0:
+            self.wait(epoch)
+            return torch.empty(x_chunk.shape, dtype=torch.float32, device=x_chunk.device) if out is None else out
+        return self.tp.finish_mailbox(x_chunk, self.mailbox, self.world, epoch, self.timeout_ns, out=out)
+
     def close(self) -> None:
         for p in self._opened:
             self.tp.lib().tp_ipc_close(p)
@@ -141,12 +163,15 @@ class PeerPairExchange:
 
 def chunk_sharded_softmax(x_chunk: torch.Tensor, out: torch.Tensor | None = None, group=None,
                           workspace: torch.Tensor | None = None,
-                          exchange: "PeerPairExchange | None" = None) -> torch.Tensor:
+                          exchange: "PeerPairExchange | None" = None, fused: bool = False) -> torch.Tensor:
     """Softmax of rows sharded by column chunk: partial -> exchange 8 B/row/rank -> finish.
 
     The exchange is one NCCL all_gather, or the one-sided NVLink mailboxes when `exchange` is
-    given."""
+    given: push / wait kernels between partial and finish, or (fused) pushed by the partial
+    kernel itself and awaited by the finish kernel itself."""
     import paper_2001_04438_b200 as tp
+    if exchange is not None and fused:
+        return exchange.finish(x_chunk, exchange.push_partial(x_chunk, workspace), out=out)
     rows = x_chunk.shape[0]
     if x_chunk.shape[-1] == 0:  # an empty trailing chunk contributes the identity (0, -inf)
         pairs = torch.tensor([[0.0, float("-inf")]] * rows, dtype=torch.float32, device=x_chunk.device)

@@ -110,3 +110,49 @@ def test_ipc_mailbox_written_by_another_process():
     assert torch.equal(allp[1], tp.partial(c1))                 # rank 1's pairs arrived through IPC
     y = np.concatenate([to_host(tp.finish(c0, allp, 2)), to_host(tp.finish(c1, allp, 2))], axis=1)
     assert np.array_equal(y, to_host(tp.softmax(xd)))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("rows,cols,dtype", [(1, 16384 * 64, "f32"), (3, 16384 * 8 + 96, "f32"),
+                                             (2, 16384 * 16, "bf16")])
+def test_fused_push_and_in_kernel_wait(world, rows, cols, dtype):
+    # softmax_partial_push_ex / softmax_finish_mailbox_ex: the partial kernel pushes its pairs and
+    # releases the flag itself, the finish kernel awaits the flags itself; emulated ranks, every
+    # partial before every finish (no kernel waits on another)
+    x = workloads.ragged_case(rows, cols, -1000, 1000, seed=22, stream=world)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    ref = to_host(tp.softmax(xd))
+    nbytes = tp.lib().tp_mailbox_bytes(world, rows)
+    boxes = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    ex = [tpd.PeerPairExchange(rows, "cuda", rank=r, world=world, mailboxes=boxes) for r in range(world)]
+    chunks = [c.contiguous() for c in _chunks(xd, world)]
+    for _ in range(3):  # epochs 1, 2, 3 on the same mailboxes
+        epochs = [ex[r].push_partial(chunks[r]) for r in range(world)]
+        outs = [to_host(ex[r].finish(chunks[r], epochs[r])) for r in range(world) if chunks[r].shape[1]]
+        assert tp.watchdog_flags() == 0 and all(e.error() == 0 for e in ex)
+        # the mailbox holds exactly the pairs the unfused partial computes
+        parts = torch.stack([tp.partial(c) if c.shape[1] else
+                             torch.tensor([[0.0, float("-inf")]] * rows, device="cuda") for c in chunks])
+        assert all(torch.equal(e.pairs(), parts) for e in ex)
+        y = np.concatenate(outs, axis=1)
+        if cols % (16384 * world) == 0:
+            assert np.array_equal(y, ref)
+        else:
+            assert_parity(x, y, f"fused W={world}")
+
+
+def test_fused_finish_times_out_instead_of_hanging():
+    rows, world = 2, 2
+    boxes = [torch.zeros(tp.lib().tp_mailbox_bytes(world, rows), dtype=torch.uint8, device="cuda")
+             for _ in range(world)]
+    ex = tpd.PeerPairExchange(rows, "cuda", rank=0, world=world, mailboxes=boxes, timeout_s=0.002)
+    xd = to_dev(workloads.ragged_case(rows, 16384 * 2, seed=23))
+    ep = ex.push_partial(xd)
+    ex.finish(xd, ep)                 # rank 1 never pushes
+    torch.cuda.synchronize()
+    assert ex.error() == 0b10
+    assert tp.watchdog_flags() & 1    # reported (and cleared) by the watchdog
+    y = tp.softmax(xd)                # the workspace is usable again afterwards
+    assert_parity(to_host(xd), to_host(y), "after timeout")
