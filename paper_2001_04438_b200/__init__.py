@@ -117,7 +117,13 @@ def _check(status: int, what: str) -> None:
         raise TwoPassError(f"{what}: {msg}")
 
 
-def _stream() -> int:
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _stream(x: torch.Tensor | None = None) -> int:
+    """The current CUDA stream (of x's device) as a raw handle."""
+    if _raw_stream is not None:
+        return _raw_stream(x.get_device() if x is not None else torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -159,13 +165,16 @@ def softmax_ex(x: torch.Tensor, algo: int = ALGO_TWO_PASS, out: torch.Tensor | N
     x = _prep(x)
     rows, cols = _rows_cols(x)
     y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
-    assert y.is_contiguous() and y.dtype == torch.float32 and y.shape == x.shape
+    if not (y.is_contiguous() and y.dtype == torch.float32 and y.shape == x.shape):
+        raise ValueError("out must be a contiguous float32 tensor of x's shape")
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel() *
                                                              workspace.element_size())
-    st = lib().softmax_ex(algo, _in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, ws_ptr, ws_bytes,
-                          _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma, schedule, cluster_size),
-                          _stream())
-    _check(st, "softmax")
+    opts = None if not (grid_ctas or lookahead_rows or force_persistent or disable_tma or schedule or cluster_size) \
+        else _opts(grid_ctas, lookahead_rows, force_persistent, disable_tma, schedule, cluster_size)
+    st = lib().softmax_ex(algo, _in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, ws_ptr, ws_bytes, opts,
+                          _stream(x))
+    if st:
+        _check(st, "softmax")
     return y
 
 
@@ -200,7 +209,7 @@ def partial(x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.T
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(),
                                                              workspace.numel() * workspace.element_size())
     st = lib().softmax_partial_ex(_in_dtype(x), x.data_ptr(), rows, cols, p.data_ptr(), ws_ptr, ws_bytes,
-                                  _opts(grid_ctas), _stream())
+                                  _opts(grid_ctas), _stream(x))
     _check(st, "partial")
     return p
 
@@ -214,7 +223,7 @@ def finish(x: torch.Tensor, pairs: torch.Tensor, world: int, out: torch.Tensor |
     assert pairs.numel() == world * rows * 2
     y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
     st = lib().softmax_finish_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, pairs.data_ptr(), world,
-                                 _opts(grid_ctas), _stream())
+                                 _opts(grid_ctas), _stream(x))
     _check(st, "finish")
     return y
 
@@ -231,7 +240,7 @@ def partial_push(x: torch.Tensor, peer_ptrs: torch.Tensor, rank: int, world: int
                                                              workspace.numel() * workspace.element_size())
     st = lib().softmax_partial_push_ex(_in_dtype(x), x.data_ptr(), rows, cols, peer_ptrs.data_ptr(), rank, world,
                                        epoch, None if pair_out is None else pair_out.data_ptr(), ws_ptr, ws_bytes,
-                                       _opts(grid_ctas), _stream())
+                                       _opts(grid_ctas), _stream(x))
     _check(st, "partial_push")
 
 
@@ -243,7 +252,7 @@ def finish_mailbox(x: torch.Tensor, mailbox: torch.Tensor, world: int, epoch: in
     rows, cols = _rows_cols(x)
     y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
     st = lib().softmax_finish_mailbox_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, mailbox.data_ptr(),
-                                         world, epoch, timeout_ns, _opts(grid_ctas), _stream())
+                                         world, epoch, timeout_ns, _opts(grid_ctas), _stream(x))
     _check(st, "finish_mailbox")
     return y
 
@@ -258,7 +267,7 @@ def phase_only(x: torch.Tensor, algo: int, phase: int, workspace: torch.Tensor,
     if y is None and not (algo == ALGO_TWO_PASS and phase == 0):
         y = torch.empty(x.shape, dtype=torch.float32, device=x.device)
     st = lib().tp_phase_only(algo, _in_dtype(x), phase, x.data_ptr(), None if y is None else y.data_ptr(), rows,
-                             cols, workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream())
+                             cols, workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream(x))
     _check(st, "phase_only")
     return y
 

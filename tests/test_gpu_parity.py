@@ -285,6 +285,11 @@ def test_small_schedule_agrees_bitwise(rows, cols, dtype):
     if cols % (8 if dtype == "bf16" else 4) == 0:       # 16-byte rows; others take the general kernel
         assert tp.last_plan()["kernel"] == "small"
     assert np.array_equal(ref, y)
+    # 1..3 CTAs per row (a cluster sharing block values through DSMEM), and few clusters
+    # looping over the rows: the same bits
+    for cl, grid in ((1, 0), (2, 0), (3, 0), (2, 6), (3, 3)):
+        yc = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_SMALL, cluster_size=cl, grid_ctas=grid))
+        assert np.array_equal(ref, yc), (cl, grid)
     if rows * cols <= 3_000_000 and rows > 1:
         assert_parity(x[1:], y[1:], "small")
 
