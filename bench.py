@@ -388,14 +388,15 @@ def main():
     three = {}
     if not args.no_three_pass and not (spec["mode"] == "chunk" and world > 1):
         for nm, algo in (("recompute", tp.ALGO_RECOMPUTE), ("reload", tp.ALGO_RELOAD)):
-            tot, _, _ = timed(lambda a=algo: tp.softmax_ex(x, a, out=y, workspace=ws), args.steps, args.warmup)
+            tot, _, _ = (timed_graph if use_graph else timed)(
+                lambda a=algo: tp.softmax_ex(x, a, out=y, workspace=ws), args.steps, args.warmup)
             ms = tot / args.steps
             three[nm] = {"ms_per_step": ms,
                          "GBps_own_cost_model": BYTES_PER_ELEM[(nm, dtype)] * elems_total / (ms * 1e-3) / 1e9,
                          "GBps_at_two_pass_bytes": value * ms_per_step / ms,
                          "two_pass_speedup": ms / ms_per_step}
         if plan["kernel"] == "cluster":  # the same Two-Pass on the grid-wide stream schedule, for context
-            tot, _, _ = timed(lambda: tp.softmax_ex(x, tp.ALGO_TWO_PASS, out=y, workspace=ws,
+            tot, _, _ = (timed_graph if use_graph else timed)(lambda: tp.softmax_ex(x, tp.ALGO_TWO_PASS, out=y, workspace=ws,
                                                     schedule=tp.SCHED_STREAM), args.steps, args.warmup)
             ms = tot / args.steps
             three["two_pass_stream_schedule"] = {"ms_per_step": ms,
