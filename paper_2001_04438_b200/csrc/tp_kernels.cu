@@ -266,9 +266,10 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
     a.prof = profile_buffer();
     if (a.vec && !o.no_tma) {
         // a few rows of 1..3 blocks: one CTA per row, the row staged in shared memory
-        if ((A == kTwoPass || A == kFused) && !o.force_persistent &&
+        // (the Three-Pass comparators too, so that they are compared on the same footing)
+        if ((A == kTwoPass || A == kFused || A == kRecompute || A == kReload) && !o.force_persistent &&
             ((o.schedule == 0 && small_applies(a.rows, a.nb, a.vec)) || (o.schedule == 4 && a.nb <= 3)))
-            return launch_small<In>(a, o, s);
+            return launch_small<In, (A == kFused ? kTwoPass : A)>(a, o, s);
         // Two-Pass rows of a few blocks: one cluster per row, pass 2 from shared memory / L2
         if (A == kTwoPass && (o.schedule == 0 || o.schedule == 3)) {
             int64_t tail = 0;

@@ -253,7 +253,7 @@ int64_t lookahead_rows(const KArgs& a, int64_t grid, int items_per_cta, const La
 template <typename In, int A>
 cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s);
 bool small_applies(int64_t rows, int64_t nb, int vec);
-template <typename In>
+template <typename In, int A>
 cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s);
 template <typename In>
 int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t* tail_rows, int* tail_ctas);

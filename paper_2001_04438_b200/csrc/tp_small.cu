@@ -95,6 +95,101 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const KArgs a, int C
     }
 }
 
+// The Three-Pass comparators on the same staging (Alg. 1 Recompute PAPER.md:88-104, Alg. 2
+// Reload PAPER.md:108-128): max pass, exchange, Sum exp pass (Reload: also y = exp(x - mu)),
+// exchange, output pass, all on the staged blocks except Reload's pass 3, which re-reads y from
+// memory as the algorithm does.  Block and row reductions are the stream kernel's (bitwise).
+template <typename In, int A>
+__global__ void __launch_bounds__(kThreads, 1) small3_kernel(const KArgs a, int CL) {
+    constexpr int V = InTraits<In>::V;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    In* stages = reinterpret_cast<In*>(dsm);
+    __shared__ __align__(8) uint64_t full_bar[kSmallMaxBlocks];
+    __shared__ Part parts[kSmallMaxBlocks];
+    __shared__ __align__(8) float2 rowvals[2][kSmallMaxBlocks * kSmallMaxCluster];  // by exchange parity
+    __shared__ float4 s_st;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nb = (int)a.nb;
+    const int q = (int)cluster_ctarank();
+    const int nloc = (nb - q + CL - 1) / CL;
+    const In* x = static_cast<const In*>(a.x);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kSmallMaxBlocks; ++b) mbar_init(&full_bar[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    unsigned iter = 0, xchg = 0;
+    // block values (warp 0) -> every cluster CTA, cluster barrier, row value (warp 0) -> s_st
+    auto exchange = [&](int phase) {
+        const int par = (int)(xchg++ & 1u);
+        if (warp == 0 && lane < nloc) {
+            const Part& pt = parts[lane];
+            float bv;
+            if (phase == 0) {
+                bv = pt.v[0].m;
+                for (int w = 1; w < kWarps; ++w) bv = fmaxf(bv, pt.v[w].m);
+            } else {
+                float t[kWarps];
+                for (int w = 0; w < kWarps; ++w) t[w] = pt.v[w].m;
+                bv = block_tree_warps_sum(t);
+            }
+            const uint32_t dst = smem_u32(&rowvals[par][q + lane * CL]);
+            for (int r = 0; r < CL; ++r) st_cluster_f2(mapa(dst, (uint32_t)r), make_float2(bv, 0.0f));
+        }
+        cluster_sync_all();
+        if (warp == 0) {
+            float root;
+            if (phase == 0) root = warp_max(lane < nb ? rowvals[par][lane].x : -__int_as_float(0x7f800000));
+            else root = warp_tree_sum(lane < nb ? rowvals[par][lane].x : 0.0f);
+            if (lane == 0) s_st = row_stats_of<A>(phase, make_float2(root, 0.0f), s_st.x);
+        }
+        __syncthreads();
+    };
+    for (int64_t row = cluster_id_x(); row < a.rows; row += nclusters_x(), ++iter) {
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            for (int j = 0; j < nloc; ++j) {
+                const int64_t e0 = (int64_t)(q + j * CL) * kBlockElems;
+                const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
+                mbar_arrive_expect_tx(&full_bar[j], bytes);
+                tma_load_1d_nohint(stages + (size_t)j * kBlockElems, x + row * a.cols + e0, bytes, &full_bar[j]);
+            }
+        }
+        for (int j = 0; j < nloc; ++j) {  // pass 1: max
+            mbar_wait_parity(&full_bar[j], iter & 1u);
+            const int valid = (int)min((int64_t)kBlockElems, a.cols - (int64_t)(q + j * CL) * kBlockElems);
+            BlockVals v;
+            load_stage<In>(stages + (size_t)j * kBlockElems, v);
+            op_max<V>(v, valid, parts[j]);
+        }
+        __syncthreads();
+        exchange(0);
+        const float mu = s_st.x;
+        for (int j = 0; j < nloc; ++j) {  // pass 2: sum of exp(x - mu)
+            const int64_t e0 = (int64_t)(q + j * CL) * kBlockElems;
+            const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
+            BlockVals v;
+            load_stage<In>(stages + (size_t)j * kBlockElems, v);
+            op_expsum<V, A == kReload>(v, valid, mu, parts[j], a.y + row * a.cols + e0, true);
+        }
+        __syncthreads();
+        exchange(1);
+        const float4 st = s_st;
+        for (int j = 0; j < nloc; ++j) {  // pass 3: output
+            const int64_t e0 = (int64_t)(q + j * CL) * kBlockElems;
+            const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
+            if (A == kRecompute) {
+                BlockVals v;
+                load_stage<In>(stages + (size_t)j * kBlockElems, v);
+                op_out_recompute<V>(v, st, a.y + row * a.cols + e0, valid, true);
+            } else {
+                op_out_reload(st, a.y + row * a.cols + e0, valid, true);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // CTAs per row: as many as the row has blocks (<= 3) while the rows still fit one wave
 static int small_cluster(int64_t rows, int64_t nb, int sms) {
     int CL = 1;
@@ -110,7 +205,7 @@ bool small_applies(int64_t rows, int64_t nb, int vec) {
     return vec && nb >= 1 && nb <= kSmallMaxBlocks && rows <= 2 * (int64_t)device_sms(dev);
 }
 
-template <typename In>
+template <typename In, int A>
 cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -121,16 +216,19 @@ cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     if (CL < 1) return cudaErrorNotSupported;
     const int per = (int)((a.nb + CL - 1) / CL);
     const size_t dyn = (size_t)per * kBlockElems * sizeof(In);
+    auto kern = A == kTwoPass ? small_kernel<In> : (A == kRecompute ? small3_kernel<In, kRecompute>
+                                                                     : small3_kernel<In, kReload>);
     static int configured[64];
     if (!configured[dev]) {
-        cudaFuncSetAttribute(small_kernel<In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kSmallMaxBlocks * kBlockElems * sizeof(In)));
+        for (auto k : {small_kernel<In>, small3_kernel<In, kRecompute>, small3_kernel<In, kReload>})
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kSmallMaxBlocks * kBlockElems * sizeof(In)));
         configured[dev] = 1;
     }
     int64_t nclu = o.grid_ctas > 0 ? o.grid_ctas / CL : sms / CL;
     if (nclu < 1) nclu = 1;
     if (nclu > a.rows) nclu = a.rows;
-    last_plan() = Plan{4, kTwoPass, nclu * CL, CL, 0, (int)a.nb};
+    last_plan() = Plan{4, A, nclu * CL, CL, 0, (int)a.nb};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(nclu * CL));
     cfg.blockDim = dim3(kThreads);
@@ -143,10 +241,14 @@ cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, small_kernel<In>, a, CL);
+    return cudaLaunchKernelEx(&cfg, kern, a, CL);
 }
 
-template cudaError_t launch_small<float>(KArgs, const LaunchOpts&, cudaStream_t);
-template cudaError_t launch_small<uint16_t>(KArgs, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_small<float, kTwoPass>(KArgs, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_small<uint16_t, kTwoPass>(KArgs, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_small<float, kRecompute>(KArgs, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_small<uint16_t, kRecompute>(KArgs, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_small<float, kReload>(KArgs, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_small<uint16_t, kReload>(KArgs, const LaunchOpts&, cudaStream_t);
 
 }  // namespace tp

@@ -290,6 +290,14 @@ def test_small_schedule_agrees_bitwise(rows, cols, dtype):
     for cl, grid in ((1, 0), (2, 0), (3, 0), (2, 6), (3, 3)):
         yc = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_SMALL, cluster_size=cl, grid_ctas=grid))
         assert np.array_equal(ref, yc), (cl, grid)
+    # the Three-Pass comparators on the same staging: bitwise equal to their stream-kernel runs
+    for algo in ("recompute", "reload"):
+        ref3 = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_STREAM))
+        for cl in (0, 1, 3):
+            y3 = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_SMALL, cluster_size=cl))
+            assert np.array_equal(ref3, y3), (algo, cl)
+        if rows * cols <= 3_000_000 and rows > 1:
+            assert_parity(x[1:], ref3[1:], f"small {algo}")
     if rows * cols <= 3_000_000 and rows > 1:
         assert_parity(x[1:], y[1:], "small")
 
