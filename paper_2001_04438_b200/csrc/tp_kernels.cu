@@ -200,8 +200,8 @@ struct SideStream {
 static SideStream g_side[64];
 
 template <typename In>
-static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_ctas, const LaunchOpts& o,
-                                cudaStream_t s) {
+static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_ctas, int side_cl,
+                                const LaunchOpts& o, cudaStream_t s) {
     if (tail > kMaxTailRows) return cudaErrorNotSupported;
     const WsLayout lt = ws_layout(tail, a.cols);
     int dev = 0;
@@ -230,7 +230,12 @@ static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_c
     if ((e = cudaStreamWaitEvent(ss.st, ss.fork, 0)) != cudaSuccess) return e;
     if ((e = launch_rowcl<In>(main, CL, o, s)) != cudaSuccess) return e;  // clusters first: they need whole GPCs
     const Plan p = last_plan();
-    if ((e = launch_stream<In, kTwoPass>(t, ot, ss.st)) != cudaSuccess) return e;
+    if (side_cl > 0) {  // the side rows on the cluster kernel (clusters of side_cl on the leftover SMs)
+        t.total_items = tail * a.nb;
+        if ((e = launch_rowcl<In>(t, side_cl, ot, ss.st)) != cudaSuccess) return e;
+    } else if ((e = launch_stream<In, kTwoPass>(t, ot, ss.st)) != cudaSuccess) {
+        return e;
+    }
     last_plan() = Plan{p.kernel, p.variant, p.grid_ctas, p.cluster_size, (int64_t)tail, p.hold};
     if ((e = cudaEventRecord(ss.join, ss.st)) != cudaSuccess) return e;
     return cudaStreamWaitEvent(s, ss.join, 0);
@@ -273,10 +278,10 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
         // Two-Pass rows of a few blocks: one cluster per row, pass 2 from shared memory / L2
         if (A == kTwoPass && (o.schedule == 0 || o.schedule == 3)) {
             int64_t tail = 0;
-            int tail_ctas = 0;
-            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size, o.schedule == 0, &tail, &tail_ctas);
+            int tail_ctas = 0, tail_cl = 0;
+            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size, o.schedule == 0, &tail, &tail_ctas, &tail_cl);
             if (CL && tail > 0) {
-                const cudaError_t e = launch_split<In>(a, CL, tail, tail_ctas, o, s);
+                const cudaError_t e = launch_split<In>(a, CL, tail, tail_ctas, tail_cl, o, s);
                 if (e != cudaErrorNotSupported) return e;
             }
             if (CL) return launch_rowcl<In>(a, CL, o, s);

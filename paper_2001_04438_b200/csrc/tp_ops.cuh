@@ -256,7 +256,8 @@ bool small_applies(int64_t rows, int64_t nb, int vec);
 template <typename In, int A>
 cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s);
 template <typename In>
-int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t* tail_rows, int* tail_ctas);
+int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t* tail_rows, int* tail_ctas,
+                 int* tail_cl);
 template <typename In>
 cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
 

@@ -526,9 +526,11 @@ static void rowcl_configure(int dev) {
 // time ~ rounds x (blocks per CTA + 1 for the row exchange); the L2 working set (pass-1 blocks
 // waiting for their pass-2 re-read, about half a row per cluster) must stay well inside L2.
 template <typename In>
-int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t* tail_rows, int* tail_ctas) {
+int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t* tail_rows, int* tail_ctas,
+                 int* tail_cl) {
     *tail_rows = 0;
     *tail_ctas = 0;
+    *tail_cl = 0;
     if (nb < 2 || nb > kClMaxNb) return 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -543,7 +545,9 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
     // 140 MB miss entirely).  The stream kernel: ~4.6 us per block over all SMs (its pipeline:
     // C4 fp32 392 us, bf16 419 us) + ~10 us of pass-1/pass-2 transition, or its DRAM traffic
     // (input twice + output) at ~6 TB/s.
-    const double in_b = (double)rows * (double)nb * kBlockElems * sizeof(In), out_b = (double)rows * nb * kBlockElems * 4.0;
+    const double row_in = (double)nb * kBlockElems * sizeof(In), row_out = (double)nb * kBlockElems * 4.0;
+    const double in_b = (double)rows * row_in, out_b = (double)rows * row_out;
+    auto miss_of = [](double foot) { return fmin(1.0, fmax(0.0, (foot - 40e6) / 100e6)); };
     int best = 0;
     double best_t = 0.0;
     for (int CL = 1; CL <= 16; CL *= 2) {
@@ -556,37 +560,54 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
         // SMs idle: the stream kernel spreads them over the whole grid instead)
         if (!force_cl && vs_stream && active * CL * 4 < (int64_t)sms * 3) continue;
         const double per_cta = (double)((nb + CL - 1) / CL);
-        const double foot = (double)active * (double)nb * kBlockElems * sizeof(In);
-        const double miss = fmin(1.0, fmax(0.0, (foot - 40e6) / 100e6));
+        const double miss = miss_of((double)active * row_in);
         const double per_round = (per_cta + 1.0) * (2.5 + 1.0 * miss);
         const double t_mem = (in_b + out_b + miss * in_b) / 6.0e6;
         const int64_t full = rows / Q, rem = rows - full * Q;
         double t = fmax((double)(full + (rem > 0)) * per_round, t_mem);
-        // tail split: the rows of a last, partly idle round go to the stream kernel on the SMs
-        // no cluster can use, concurrently (shared DRAM counted).  Moving more rows than that to
-        // the stream launch measured no faster (C4: 1 row 368-373 us, 31 rows 372 us).
+        // Side launch on the SMs no cluster of this size can use, concurrent with the cluster
+        // launch (shared DRAM counted): the rows beyond F full rounds of the clusters.  On the
+        // cluster kernel with the smallest cluster a row allows (CL 2 for C4: clusters of two
+        // fit the leftover SMs of a GPC), else on the stream kernel (then only the last round's
+        // rows: more measured no faster).  C4 fp32: F = 16 rounds + 16 side rows on 14 pairs,
+        // 351 us against 358 with the last row on the stream kernel.
         const int64_t idle = (int64_t)sms - (int64_t)Q * CL;
         int64_t split = 0;
+        int split_cl = 0;
         static const int env_split = [] {  // development: TP_CL_SPLIT=1 also splits forced sizes
             const char* e = getenv("TP_CL_SPLIT");
             return e ? atoi(e) : 0;
         }();
         if ((env_split || (!force_cl && vs_stream)) && full > 0 && idle >= 8) {
-            const double row_in = (double)nb * kBlockElems * sizeof(In), row_out = (double)nb * kBlockElems * 4.0;
-            for (int64_t F = full; F >= 1 && F >= full; --F) {
+            int cls = 1;
+            while ((nb + cls - 1) / cls > kClMaxLocal) cls *= 2;
+            if (cls > 2 || max_active_clusters<In>(dev, cls, dyn) < 1) cls = 0;  // stream side launch
+            const int64_t qs = cls ? idle / cls : idle;
+            // at most one round of the clusters moves to the side launch (more measured slower:
+            // the side rows' L2 footprint and DRAM traffic slow the clusters down)
+            for (int64_t F = full; F >= 1 && F >= full - (cls ? 1 : 0); --F) {
                 const int64_t T = rows - F * Q;
                 if (T <= 0 || T > 256) continue;
-                const double t_tail = (double)T * (double)nb / (double)idle * 4.6 + 15.0;
-                const double dram = ((double)(F * Q) * (row_in * (1.0 + miss) + row_out) +
-                                     (double)T * (2.0 * row_in + row_out)) / 6.0e6;
-                const double t_split = fmax(fmax((double)F * per_round, t_tail), dram);
-                if (t_split < t || (env_split && split == 0)) t = t_split, split = T;
+                double t_side, side_dram;
+                if (cls) {
+                    const double miss_s = miss_of((double)(T < qs ? T : qs) * row_in);
+                    const double rounds = (double)((T + qs - 1) / qs);
+                    t_side = rounds * (double)((nb + cls - 1) / cls + 1) * (2.5 + 1.0 * miss_s);
+                    side_dram = (double)T * (row_in * (1.0 + miss_s) + row_out);
+                } else {
+                    t_side = (double)T * (double)nb / (double)idle * 4.6 + 15.0;
+                    side_dram = (double)T * (2.0 * row_in + row_out);
+                }
+                const double dram = ((double)(F * Q) * (row_in * (1.0 + miss) + row_out) + side_dram) / 6.0e6;
+                const double t_split = fmax(fmax((double)F * per_round, t_side), dram);
+                if (t_split < t || (env_split && split == 0)) t = t_split, split = T, split_cl = cls;
             }
         }
         if (best == 0 || t < best_t) {
             best = CL, best_t = t;
             *tail_rows = split;
             *tail_ctas = split ? (int)idle : 0;
+            *tail_cl = split ? split_cl : 0;
         }
     }
     if (best && vs_stream) {
@@ -594,6 +615,7 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
         if (t_st < best_t) {
             *tail_rows = 0;
             *tail_ctas = 0;
+            *tail_cl = 0;
             return 0;
         }
     }
@@ -640,8 +662,8 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, SA, LA);
 }
 
-template int rowcl_choose<float>(int64_t, int64_t, int, bool, int64_t*, int*);
-template int rowcl_choose<uint16_t>(int64_t, int64_t, int, bool, int64_t*, int*);
+template int rowcl_choose<float>(int64_t, int64_t, int, bool, int64_t*, int*, int*);
+template int rowcl_choose<uint16_t>(int64_t, int64_t, int, bool, int64_t*, int*, int*);
 template cudaError_t launch_rowcl<float>(KArgs, int, const LaunchOpts&, cudaStream_t);
 template cudaError_t launch_rowcl<uint16_t>(KArgs, int, const LaunchOpts&, cudaStream_t);
 
