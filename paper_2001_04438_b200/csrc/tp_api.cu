@@ -121,6 +121,8 @@ bool overlap_bad(const void* x, size_t xbytes, const void* y, size_t ybytes, boo
 
 int check_args(int in_dtype, const void* x, const float* y, int64_t rows, int64_t cols, bool need_y) {
     if (!x || (need_y && !y)) return TP_EINVAL;
+    int dev;  // a usable device, and one the per-device tables (kMaxDev entries) cover
+    if (const int st = current_device(&dev)) return st;
     if (rows < 1 || cols < 1) return TP_EINVAL;
     if (in_dtype != TP_IN_F32 && in_dtype != TP_IN_BF16) return TP_EINVAL;
     if (rows > (int64_t(1) << 40) / cols) return TP_EINVAL;  // 2^40 elements: far beyond HBM
