@@ -12,8 +12,10 @@ struct WsHeader {
     unsigned long long counter;  // next work item
     unsigned exit_ticket;        // CTAs that left the kernel
     unsigned epoch;              // launches completed; row flags are valid when == epoch + 1
-    unsigned error;              // watchdog: bit 0 = a wait for a row flag timed out
     unsigned rows_done;          // kPartial with a fused push: rows whose pair has been pushed
+    // watchdog: bit 0 = a wait for a row flag timed out.  Its own 128-byte line: every role
+    // polls it while waiting, and the work-queue atomics on `counter` must not queue behind them
+    alignas(128) unsigned error;
 };
 
 // Mailbox of the one-sided pair exchange: uint32 flags[world] at 0, error word at byte 240, then

@@ -135,38 +135,54 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         long long pushed = 0;
         // per stage, in registers: parity of the next use (bit s of use_par), state (2 bits: 0 free,
         // 1 busy until its empty barrier completes, 2 waiting for stats, 3 retired (hold mode:
-        // its reservation was past the end)), issue sequence of its item (order[], local)
-        unsigned use_par = 0, st_bits = 0;
+        // its reservation was past the end)); the stages waiting for stats in issue order, oldest
+        // in the low nibble of wq (wn entries): their commands are pushed in that order
+        unsigned use_par = 0, st_bits = 0, wq = 0;
+        int wn = 0;
         auto state_of = [&](int s) -> int { return (int)((st_bits >> (2 * s)) & 3u); };
         auto set_state = [&](int s, int v) { st_bits = (st_bits & ~(3u << (2 * s))) | ((unsigned)v << (2 * s)); };
-        long long order[S];    // issue sequence of the stage's item (stats are provided in this order)
+        auto wait_stats = [&](int s) {  // stage s now waits for its row statistics
+            set_state(s, 2);
+            wq |= (unsigned)s << (4 * wn);
+            ++wn;
+        };
         // hold mode: each stage owns one reservation, taken when the stage is certain to free
         // without waiting on anything (at start, and when its P2 command is pushed).  A CTA
         // never reserves a block it cannot stage, so the oldest unreleased row always gets all
         // its blocks staged (a row must not wait on a block queued behind held stages).
         unsigned long long resv[S];
-        for (int s = 0; s < S; ++s) order[s] = 0;
         if (hold)
             for (int s = 0; s < S; ++s) resv[s] = atomicAdd(&hdr->counter, 1ull);
-        long long issue_seq = 0;
+        long long dec_item = -2;  // the last decoded stream item (the next one is usually its neighbour)
+        Item dec_it{0, 0, 0};
         int64_t cached_row = -1;
         int cached_phase = -1;
         float4 cached_st = make_float4(0.f, 0.f, 0.f, 0.f);
         unsigned long long wait_t0 = 0;
 
+        // development (KArgs::prof): producer cycle accounting, summed over CTAs into prof[8..13] =
+        // chunk switches (waiting for the prefetched atomic), issue, command-slot waits, loop
+        // passes without an issue, total, items issued
+        unsigned long long ppc[6] = {0, 0, 0, 0, 0, 0};
+        unsigned long long pfx[2] = {0, 0};  // proxy fence, expect_tx + bulk copy issue
+        const unsigned long long ppc_start = a.prof ? clock64() : 0ull;
         auto take = [&]() -> long long {
             if (next == end) {
+                const unsigned long long c0 = a.prof ? clock64() : 0ull;
                 next = ahead;
                 end = next + kChunk;
                 ahead = atomicAdd(&hdr->counter, kChunk);
+                if (a.prof) ppc[0] += clock64() - c0;
             }
             return (long long)next++;
         };
 
         auto push = [&](int op, int s, unsigned parity) {
             const int c = (int)(pushed % C);
+            const unsigned long long c0 = a.prof ? clock64() : 0ull;
             if (pushed >= C && !wait_or_abort(&cempty_bar[c], (uint32_t)(((pushed / C) - 1) & 1), &hdr->error, 64u))
                 return;
+            if (a.prof) ppc[2] += clock64() - c0;
             cmds[c] = Cmd{op, s, parity};
             mbar_arrive(&cfull_bar[c]);
             ++pushed;
@@ -194,11 +210,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
 
         // push the commands whose statistics are now available, oldest item first
         auto poll = [&]() {
-            for (;;) {
-                int best = -1;
-                for (int s = 0; s < S; ++s)
-                    if (state_of(s) == 2 && (best < 0 || order[s] < order[best])) best = s;
-                if (best < 0) return;
+            while (wn > 0) {
+                const int best = (int)(wq & 15u);
                 const Item it = meta[best].it;
                 float4 st;
                 if (!stats_ready(it, hold ? 0 : it.phase - 1, &st)) return;
@@ -207,6 +220,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                                       ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) +
                                                it.row * a.nb + it.blk)
                                       : 0u;
+                wq >>= 4;
+                --wn;
                 set_state(best, 1);
                 push(hold ? kOpP2 : kOpItem, best, ((use_par >> best) & 1u) ^ 1u);
                 if (hold) resv[best] = atomicAdd(&hdr->counter, 1ull);  // consumed when the stage frees
@@ -221,9 +236,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 it.row = u / nb;
                 it.blk = u - (u / nb) * nb;
                 if (it.phase > 0) it.blk = a.nb - 1 - it.blk;
+            } else if (item == dec_item + 1 && (uint64_t)item % (uint64_t)a.nb != 0) {
+                it = dec_it;  // the next block of the same (row, phase) unit (decode_item's direction)
+                it.blk += (A == kFinish || it.phase > 0) ? -1 : 1;
             } else {
                 it = decode_item<A>(item, a.rows, a.nb, a.L);
             }
+            if (!hold && !a.phase_only) dec_item = item, dec_it = it;
             const int64_t e0 = it.blk * kBlockElems;
             const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
             meta[s].item = item;
@@ -231,17 +250,19 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
             meta[s].valid = valid;
             const unsigned parity = (use_par >> s) & 1u;
             use_par ^= 1u << s;
-            order[s] = issue_seq++;
             if (A == kReload && it.phase == 2) {  // Reload's pass 3 reads Y, not X: no copy
                 mbar_arrive(&full_bar[s]);
             } else {
                 const uint32_t bytes = (uint32_t)valid * (uint32_t)sizeof(In);
                 const bool keep = !hold && !a.phase_only && ((P > 1 && it.phase < P - 1) || A == kPartial);
                 In* dst = stages + (size_t)s * kBlockElems;
+                const unsigned long long f0 = a.prof ? clock64() : 0ull;
                 fence_proxy_async_smem();
+                const unsigned long long f1 = a.prof ? clock64() : 0ull;
                 mbar_arrive_expect_tx(&full_bar[s], bytes);
                 if (a.l2_hints) tma_load_1d(dst, x + it.row * a.cols + e0, bytes, &full_bar[s], keep ? pol_keep : pol_drop);
                 else tma_load_1d_nohint(dst, x + it.row * a.cols + e0, bytes, &full_bar[s]);
+                if (a.prof) pfx[0] += f1 - f0, pfx[1] += clock64() - f1;
             }
             if (A == kFinish) {
                 if (it.row != cached_row) {
@@ -252,11 +273,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 meta[s].mask = 0xffffffffu;  // the chunk's pass-1 clamp decisions are not known here
             }
             if (hold) {
-                set_state(s, 2);  // P1 now, P2 once the row is released
+                wait_stats(s);  // P1 now, P2 once the row is released
                 push(kOpP1, s, parity);
             } else if (item_needs_stats<A>(it) && A != kFinish) {
                 if (a.prof && tl_p2 == 0) tl_p2 = globaltimer_ns();
-                set_state(s, 2);
+                wait_stats(s);
                 poll();
             } else {
                 set_state(s, 1);
@@ -265,10 +286,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
         };
 
         if (A == kFinish && a.mailbox) finish_wait(a);  // fused NVLink exchange: the peers' pairs
-        for (;;) {
-            if (aborted(&hdr->error)) return;  // watchdog: every role leaves
-            poll();
-            bool busy = false;
+        for (unsigned pass = 0;; ++pass) {
+            // watchdog: every role leaves.  Polled every 64 passes: the flag shares the header
+            // with the work-queue counter every producer's atomics hit
+            if ((pass & 63u) == 63u && aborted(&hdr->error)) return;
+            if (wn > 0) poll();
+            bool busy = false, issued_now = false;
             for (int s = 0; s < S; ++s) {
                 if (state_of(s) == 1 && mbar_test_parity(&empty_bar[s], ((use_par >> s) & 1u) ^ 1u)) set_state(s, 0);
                 if (hold) {
@@ -284,17 +307,26 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                     if (item >= total) {
                         exhausted = true;
                         if (a.prof) tl_exh = globaltimer_ns();
+                    } else {
+                        const unsigned long long c0 = a.prof ? clock64() : 0ull;
+                        issue(s, item);
+                        if (a.prof) ppc[1] += clock64() - c0, ppc[5] += 1;
+                        issued_now = true;
                     }
-                    else issue(s, item);
                 }
                 busy |= state_of(s) != 0;
             }
             if ((hold || exhausted) && !busy) break;
+            if (a.prof && !issued_now) ppc[3] += 1;
 
         }
         push(kOpExit, 0, 0);
         if (!hold && ahead == ~0ull) hdr->error |= 2u;  // consume the last prefetch before leaving
         if (a.prof) {
+            ppc[4] = clock64() - ppc_start;
+            for (int i = 0; i < 6; ++i) atomicAdd(&a.prof[8 + i], ppc[i]);
+            atomicAdd(&a.prof[14], pfx[0]);
+            atomicAdd(&a.prof[15], pfx[1]);
             unsigned long long* t = a.prof + 16 + 5 * blockIdx.x;
             t[0] = tl_start;
             t[1] = tl_exh;

@@ -42,12 +42,16 @@ run()
 e.record()
 e.synchronize()
 tp.lib().tp_set_profile_buffer(None)
-b = buf.cpu().tolist()[:8]
+bb = buf.cpu().tolist()
+b = bb[:8]
+prod = dict(zip(["chunk_switch", "issue", "cmd_slot_wait", "idle_passes", "total", "issued", "proxy_fence",
+                "copy_issue"], bb[8:16]))
 ctas = sum(1 for v in buf.cpu().numpy()[16:].reshape(-1, 5)[:, 0] if v > 0) or 1
 blocks = max(b[6] + b[7], 1)
 out = {"config": key, "what": what, "event_us": round(s.elapsed_time(e) * 1e3, 1), "ctas": ctas,
        "per_cta_kcycles": {k: round(v / ctas / 1e3, 1) for k, v in zip(SLOTS[:6], b[:6])},
        "per_block_cycles": {k: round(v / blocks) for k, v in zip(SLOTS[:6], b[:6])},
        "p1_ops_per_p1_block": round(b[3] / max(b[6], 1)), "p2_ops_per_p2_block": round(b[4] / max(b[7], 1)),
-       "blocks": {"p1": b[6], "p2": b[7]}}
+       "blocks": {"p1": b[6], "p2": b[7]},
+       "producer_per_item_cycles": {k: round(v / max(prod["issued"], 1)) for k, v in prod.items() if k != "issued"}}
 print(json.dumps(out))
