@@ -187,10 +187,13 @@ static cudaError_t launch_general(KArgs a, const LaunchOpts& o, cudaStream_t s) 
     return cudaGetLastError();
 }
 
-// Cluster kernel on the first rows - tail rows, the stream kernel on the tail rows on the SMs the
-// clusters leave idle, concurrently: fork / join on an internal side stream with events (graph
-// capturable).  The tail uses the workspace's tail layout (tail_ws_offset).
-// cudaErrorNotSupported for a tail longer than that layout: the caller runs the plain launch.
+// Cluster kernel on the first rows - tail rows; the tail rows on the SMs the clusters leave idle,
+// concurrently (the cluster kernel in clusters of side_cl, or the stream kernel when side_cl is
+// 0): fork / join on an internal per-device side stream with events (graph capturable; callers
+// on different streams share it, which orders their side launches but not their results).  The
+// tail uses the workspace's tail layout (tail_ws_offset).  cudaErrorNotSupported for a tail
+// longer than that layout: the caller runs the plain launch.  Should the side launch fail, the
+// tail rows run on the caller's stream after the main launch instead.
 
 struct SideStream {
     std::mutex mu;
@@ -230,15 +233,19 @@ static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_c
     if ((e = cudaStreamWaitEvent(ss.st, ss.fork, 0)) != cudaSuccess) return e;
     if ((e = launch_rowcl<In>(main, CL, o, s)) != cudaSuccess) return e;  // clusters first: they need whole GPCs
     const Plan p = last_plan();
-    if (side_cl > 0) {  // the side rows on the cluster kernel (clusters of side_cl on the leftover SMs)
-        t.total_items = tail * a.nb;
-        if ((e = launch_rowcl<In>(t, side_cl, ot, ss.st)) != cudaSuccess) return e;
-    } else if ((e = launch_stream<In, kTwoPass>(t, ot, ss.st)) != cudaSuccess) {
-        return e;
-    }
+    KArgs ts = t;
+    ts.total_items = tail * a.nb;
+    const cudaError_t e_side =
+        side_cl > 0 ? launch_rowcl<In>(ts, side_cl, ot, ss.st) : launch_stream<In, kTwoPass>(t, ot, ss.st);
     last_plan() = Plan{p.kernel, p.variant, p.grid_ctas, p.cluster_size, (int64_t)tail, p.hold};
-    if ((e = cudaEventRecord(ss.join, ss.st)) != cudaSuccess) return e;
-    return cudaStreamWaitEvent(s, ss.join, 0);
+    e = cudaEventRecord(ss.join, ss.st);  // the fork is always joined
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ss.join, 0);
+    if (e != cudaSuccess || e_side == cudaSuccess) return e;
+    cudaGetLastError();  // the side launch was refused: the tail rows on s, after the main launch
+    LaunchOpts oq = o;
+    oq.schedule = 1;
+    oq.grid_ctas = 0;
+    return launch_stream<In, kTwoPass>(t, oq, s);
 }
 
 template <typename In, int A>
