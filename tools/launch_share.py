@@ -12,13 +12,15 @@ def main(path):
     rows = list(csv.reader(lines))
     h = rows[0]
     ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    gi = h.index("Grid Size") if "Grid Size" in h else None
     per = collections.defaultdict(dict)
     for r in rows[1:]:
         per[int(r[ii])][r[mi]] = float(r[vi].replace(",", ""))
-        per[int(r[ii])]["k"] = r[ki]
+        # one line per kernel and grid: e.g. the cluster launch and its concurrent side launch
+        per[int(r[ii])]["k"] = r[ki].split("(")[0][:60] + (f" grid={r[gi].strip('()').split(',')[0]}" if gi is not None else "")
     tot, cnt, by = collections.Counter(), collections.Counter(), collections.Counter()
     for d in per.values():
-        k = d["k"].split("(")[0][:70]
+        k = d["k"]
         tot[k] += d.get("gpu__time_duration.sum", 0)
         cnt[k] += 1
         by[k] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
