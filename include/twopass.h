@@ -196,7 +196,7 @@ int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t c
  * kernel = 1 general (any alignment), 2 stream (persistent grid), 3 cluster (one
  * thread-block cluster per row), 4 small (one CTA per row of <= 3 blocks); variant = the kernel's operation (0 Two-Pass, 1 partial,
  * 2 Recompute, 3 Reload, 4 single-block rows, 5 finish); grid_ctas; cluster_size (kernel 3);
- * lookahead_rows (kernel 1/2; kernel 3: rows handed to a concurrent stream launch on the SMs
+ * lookahead_rows (kernel 1/2; kernel 3: rows handed to a concurrent side launch on the SMs
  * the clusters leave idle, 0 if none); hold (kernel 2: blocks kept staged between the passes;
  * kernel 3: half-stages of the pass-1 pool).  Returns TP_EINVAL for a NULL pointer. */
 typedef struct {

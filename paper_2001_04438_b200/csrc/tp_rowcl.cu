@@ -657,7 +657,7 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     constexpr int S2 = ClRing<In>::S2;
     const int SA = env_sa >= 2 && env_sa <= S2 - 2 ? env_sa : S2 / 2;
     const int LA = env_la >= 1 ? env_la : 1;
-    last_plan() = Plan{3, kTwoPass, ncl * CL, CL, LA, SA};
+    last_plan() = Plan{3, kTwoPass, ncl * CL, CL, 0, SA};  // lookahead_rows: side rows (launch_split)
     if (a.prof) return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, true>, a, CL, SA, LA);
     return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, SA, LA);
 }
