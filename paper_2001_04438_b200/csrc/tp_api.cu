@@ -6,6 +6,7 @@
 
 #include <cuda.h>
 #include <mutex>
+#include <vector>
 #include <unordered_map>
 #include <utility>
 
@@ -317,9 +318,31 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
             d.hws_bytes = wsb;
         }
     }
-    for (int64_t r0 = 0, i = 0; r0 < rows; r0 += slab, ++i) {
-        const int k = (int)(i % nstreams);
-        const int64_t nr = rows - r0 < slab ? rows - r0 : slab;
+    // Slab sizes: full slabs in the middle, a doubling ramp at both ends (slab/8, /4, /2 ...) so
+    // that the first H2D copy and the last D2H copy, which nothing overlaps, are short.
+    static const int ramp = [] {  // development override TP_HOST_RAMP=0: equal slabs
+        const char* e = getenv("TP_HOST_RAMP");
+        return e ? atoi(e) : 1;
+    }();
+    std::vector<int64_t> sizes;
+    {
+        std::vector<int64_t> up;
+        int64_t ramp_rows = 0;
+        if (ramp)
+            for (int64_t z = slab / 8 > 0 ? slab / 8 : 1; z < slab; z *= 2) up.push_back(z), ramp_rows += 2 * z;
+        if (!ramp || rows < ramp_rows + 2 * slab) {
+            for (int64_t r0 = 0; r0 < rows; r0 += slab) sizes.push_back(rows - r0 < slab ? rows - r0 : slab);
+        } else {
+            sizes = up;
+            int64_t mid = rows - ramp_rows;
+            for (; mid > 0; mid -= slab) sizes.push_back(mid < slab ? mid : slab);
+            sizes.insert(sizes.end(), up.rbegin(), up.rend());
+        }
+    }
+    int64_t r0 = 0;
+    for (size_t i = 0; i < sizes.size(); r0 += sizes[i], ++i) {
+        const int k = (int)(i % (size_t)nstreams);
+        const int64_t nr = sizes[i];
         cudaStream_t s = d.st[k];
         e = cudaMemcpyAsync(d.hx_dev[k], (const char*)hx + (size_t)(r0 * cols) * esz, (size_t)(nr * cols) * esz,
                             cudaMemcpyHostToDevice, s);
