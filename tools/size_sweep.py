@@ -4,7 +4,8 @@ sweeps and F8/F9 thread scaling).
     python tools/size_sweep.py [--json out.json]
 
 1. Single rows of N = 2^10 .. 2^30 fp32 elements: Two-Pass vs Three-Pass (Recompute, Reload),
-   under two cache protocols: "cold" (512 MB L2 flush before every rep) and "warm" (no flush:
+   under two cache protocols: "cold" (512 MB write + read before every rep: L2 holds clean,
+   unrelated lines) and "warm" (no flush:
    input and output stay in L2 while they fit - the GPU analogue of PAPER.md:228's protocol,
    whose output eviction has no direct GPU counterpart since writes allocate in L2 too).
 2. SM-count scaling: C4 (256 x 800,000 fp32) with the persistent grid capped at 1..148 CTAs
@@ -72,6 +73,12 @@ def main():
     ap.add_argument("--max-log2", type=int, default=30)
     args = ap.parse_args()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    f32 = flush.view(torch.float32)
+
+    def clean_flush():  # write 512 MB, then read it: L2 left holding clean lines only
+        flush.zero_()
+        tp.lib().tp_stream_baseline(4, f32.data_ptr(), f32.data_ptr(), f32.numel(), 1.0, 0, tp._stream())
+
     out = {"size_sweep": [], "sm_scaling": []}
     for lg in range(10, args.max_log2 + 1):
         n = 1 << lg
@@ -80,7 +87,7 @@ def main():
         reps = 25 if n <= (1 << 24) else 7
         for name, algo, bpe in ALGOS:
             fn = (lambda a=algo: tp.softmax_ex(x, a, out=y))
-            t_cold = timed(fn, lambda: flush.zero_(), reps)
+            t_cold = timed(fn, clean_flush, reps)
             t_warm = timed(fn, lambda: None, reps)
             rec = {"n": n, "algo": name, "cold_us": t_cold * 1e6, "cold_GBps": bpe * n / t_cold / 1e9,
                    "warm_us": t_warm * 1e6, "warm_GBps": bpe * n / t_warm / 1e9}
@@ -94,7 +101,7 @@ def main():
     x = torch.from_numpy(workloads.generate("c4")).cuda()
     y = torch.empty_like(x)
     for g in (1, 2, 4, 8, 16, 32, 64, 96, 128, 148):
-        t = timed(lambda: tp.softmax_ex(x, out=y, grid_ctas=g, schedule=tp.SCHED_STREAM), lambda: flush.zero_(), 5)
+        t = timed(lambda: tp.softmax_ex(x, out=y, grid_ctas=g, schedule=tp.SCHED_STREAM), clean_flush, 5)
         rec = {"ctas": g, "us": t * 1e6, "GBps": 12 * x.numel() / t / 1e9}
         out["sm_scaling"].append(rec)
         print(json.dumps(rec), flush=True)
