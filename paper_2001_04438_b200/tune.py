@@ -17,7 +17,7 @@ import threading
 
 import torch
 
-from . import (ALGO_TWO_PASS, SCHED_AUTO, SCHED_CLUSTER, SCHED_HOLD, SCHED_STREAM, softmax_ex)
+from . import (ALGO_TWO_PASS, SCHED_AUTO, SCHED_CLUSTER, SCHED_HOLD, SCHED_SMALL, SCHED_STREAM, softmax_ex)
 
 _LOCK = threading.Lock()
 DEFAULT_CACHE = os.path.join(os.path.expanduser("~"), ".cache", "paper_2001_04438_b200", "tune.json")
@@ -32,6 +32,8 @@ def candidates(rows: int, cols: int) -> list[dict]:
         c += [dict(schedule=SCHED_HOLD)]
     if 2 <= nb <= 256:
         c += [dict(schedule=SCHED_CLUSTER, cluster_size=cl) for cl in (1, 2, 4, 8) if cl <= nb]
+    if nb <= 3:  # rows staged whole in 1..3 CTAs
+        c += [dict(schedule=SCHED_SMALL, cluster_size=cl) for cl in (1, 2, 3) if cl <= nb]
     return c
 
 

@@ -9,7 +9,11 @@ tp = pytest.importorskip("paper_2001_04438_b200")
 
 def test_candidates_cover_the_schedules_that_apply():
     one_block = tune.candidates(64, 1000)
-    assert {"schedule": tp.SCHED_AUTO} in one_block and all("cluster_size" not in c for c in one_block)
+    assert {"schedule": tp.SCHED_AUTO} in one_block
+    assert all(c["schedule"] != tp.SCHED_CLUSTER for c in one_block)
+    assert {c.get("cluster_size") for c in one_block if c["schedule"] == tp.SCHED_SMALL} == {1}
+    two_blocks = tune.candidates(64, 32768)  # C2: the small schedule with 1 or 2 CTAs per row
+    assert {c.get("cluster_size") for c in two_blocks if c["schedule"] == tp.SCHED_SMALL} == {1, 2}
     c4 = tune.candidates(256, 800000)       # 49 blocks per row: cluster sizes 1..8, look-aheads
     assert {c.get("cluster_size") for c in c4 if c["schedule"] == tp.SCHED_CLUSTER} == {1, 2, 4, 8}
     assert any(c.get("lookahead_rows") == 32 for c in c4)
