@@ -172,7 +172,9 @@ int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64
  *   LOCAL mailbox equal `epoch`; a flag missing for timeout_ns sets its rank's bit in the
  *   mailbox error word and watchdog bit 0 (outputs then undefined; nothing hangs).
  * Sequence per rank: partial_push -> finish_mailbox, two launches, no NCCL, no host
- * synchronisation.  Results are bit-identical to partial -> all_gather -> finish.
+ * synchronisation.  Results are bit-identical to partial -> all_gather -> finish.  The epoch is
+ * a launch argument: a captured CUDA graph replays the same epoch, so a graph must be captured
+ * per epoch (or the mailboxes zeroed between replays) for its waits to mean anything.
  * TP_EINVAL: bad sizes / pointers, world outside 1..56, rank outside [0, world), epoch 0,
  * mailbox not 16-byte aligned.  Asynchronous. */
 int softmax_partial_push_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, void* const* peer_mailboxes,
