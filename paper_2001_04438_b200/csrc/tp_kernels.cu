@@ -293,6 +293,19 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
             }
             if (CL) return launch_rowcl<In>(a, CL, o, s);
         }
+        // the Three-Pass comparators on a one-cluster-per-row schedule (tp_rowcl3.cu; opt-in:
+        // faster than their stream schedule for some algorithm / dtype pairs on C4, slower for
+        // others, so bench.py times both and compares against the faster)
+        if ((A == kRecompute || A == kReload) && o.schedule == 3) {
+            int64_t tail = 0;
+            int tail_ctas = 0, tail_cl = 0;
+            const int CL = rowcl_choose<In>(a.rows, a.nb, o.cluster_size, false, &tail, &tail_ctas, &tail_cl);
+            if (CL) {
+                const cudaError_t e = launch_rowcl3<In, (A == kReload ? kReload : kRecompute)>(a, CL, o, s);
+                if (e != cudaErrorNotSupported) return e;
+                cudaGetLastError();
+            }
+        }
         return launch_stream<In, A>(a, o, s);
     }
     return launch_general<In, A>(a, o, s);

@@ -260,5 +260,7 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
                  int* tail_cl);
 template <typename In>
 cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
+template <typename In, int A>
+cudaError_t launch_rowcl3(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
 
 }  // namespace tp

@@ -539,3 +539,23 @@ def test_phase_only_rejects_bad_arguments():
     with pytest.raises(tp.TwoPassError):  # misaligned rows: the stream kernel only
         xm = to_dev(workloads.ragged_case(2, 16384 + 3, seed=18))
         tp.phase_only(xm, tp.ALGO_TWO_PASS, 0, tp.new_workspace(*xm.shape))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", [(40, 800000), (7, 16384 * 2 + 36), (20, 16384 * 100 + 8), (150, 16384 * 9),
+                                       (3, 16384 * 256)])
+def test_three_pass_cluster_schedule_agrees_bitwise(rows, cols, dtype):
+    # the comparators on the one-cluster-per-row schedule (tp_rowcl3.cu): the stream kernel's
+    # bits for every cluster size, and the oracle's tolerance
+    x = workloads.ragged_case(rows, cols, -300, 300, seed=20, stream=rows + cols)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    for algo in ("recompute", "reload"):
+        ref = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_STREAM))
+        for cl in (0, 2, 8):
+            y = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_CLUSTER, cluster_size=cl))
+            assert np.array_equal(ref, y), (algo, cl, tp.last_plan())
+        assert tp.watchdog_flags() == 0
+        if rows * cols <= 8_000_000:
+            assert_parity(x, ref, f"{algo} cluster")
