@@ -460,7 +460,10 @@ def main():
                          "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload, kernel_name),
                          "kernel": kernel_name, "plan": plan,
                          "algorithmic_bytes_per_launch": per_elem * n_local,
-                         "launch_ms_mean": launch_ms, "peak_source": peak_src},
+                         "launch_ms_mean": launch_ms, "peak_source": peak_src,
+                         "note": ("achieved counts the paper's compulsory bytes (2 reads + 1 write per element); "
+                                  "the DRAM traffic per launch (traffic) is lower where pass-2 re-reads hit L2 / "
+                                  "shared memory, so frac can exceed 1")},
             "three_pass": three or None,
             "cpu_baseline": cpu,
             "e2e": e2e,
