@@ -130,10 +130,11 @@ int tp_ipc_close(void* dev_ptr);
  *   bulk copies into shared memory; schedule = TP_SCHED_AUTO (0), TP_SCHED_STREAM (1:
  *   a persistent grid shares every row, pass-2 blocks are re-read from L2/HBM),
  *   TP_SCHED_HOLD (2: as STREAM, but Two-Pass rows of a few blocks stay staged in shared
- *   memory between the passes) or TP_SCHED_CLUSTER (3: Two-Pass rows of 2..256 blocks,
- *   one thread-block cluster per row, the row's block values exchanged through distributed
- *   shared memory, pass 2 from shared memory / L2; AUTO picks it when the cluster's L2
- *   working set fits); a schedule that does not apply falls back to STREAM;
+ *   memory between the passes) or TP_SCHED_CLUSTER (3: rows of 2..256 blocks, one
+ *   thread-block cluster per row, the row's block values exchanged through distributed
+ *   shared memory, the re-reads from shared memory / L2; AUTO picks it for the Two-Pass
+ *   when the cluster's L2 working set fits; for the Three-Pass comparators only on request);
+ *   a schedule that does not apply falls back to STREAM;
  *   cluster_size = CTAs per row for TP_SCHED_CLUSTER (0 = automatic; 1, 2, 4, 8 or 16).
  *   Results do not depend on any of these (bit-identical outputs). */
 #define TP_SCHED_AUTO 0
