@@ -2,8 +2,9 @@
 
     python tools/stress.py c4:two_pass c4b:two_pass:schedule=2 --reps 50
 
-For each spec: `reps` launches, each timed with CUDA events and followed by a synchronise and
-a watchdog-flag read (reset on error); prints the time distribution and every failing launch.
+For each spec: `reps` launches, each timed with CUDA events and followed by a synchronise, a
+watchdog-flag read (reset on error) and a bitwise comparison with the first launch's output;
+prints the time distribution and every failing launch.
 """
 import argparse
 import json
@@ -39,7 +40,7 @@ def main():
                           if x.dtype == np.uint16 else torch.from_numpy(x).cuda())
         xd = cache[key]
         y = torch.empty(xd.shape, dtype=torch.float32, device="cuda")
-        ts, bad = [], []
+        ts, bad, ref = [], [], None
         for i in range(args.reps):
             if args.flush:
                 flush.zero_()
@@ -50,8 +51,11 @@ def main():
             e.synchronize()
             ts.append(s.elapsed_time(e) * 1e3)
             f = tp.watchdog_flags()
-            if f:
-                bad.append((i, f, ts[-1]))
+            if ref is None:
+                ref = y.clone()
+            same = bool(torch.equal(y, ref))
+            if f or not same:
+                bad.append((i, f, same, ts[-1]))
         ts = np.array(ts)
         print(json.dumps(dict(spec=spec, median_us=float(np.median(ts)), min_us=float(ts.min()),
                               max_us=float(ts.max()), p90_us=float(np.percentile(ts, 90)), n_bad=len(bad), plan=tp.last_plan(),
