@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const KArgs a, int C
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait_and_release();  // programmatic launch: set up above, touch memory only after the predecessor
     unsigned iter = 0;
     for (int64_t row = cluster_id_x(); row < a.rows; row += nclusters_x(), ++iter) {
         if (threadIdx.x == 0) {
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1) small3_kernel(const KArgs a, int 
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait_and_release();
     unsigned iter = 0, xchg = 0;
     // block values (warp 0) -> every cluster CTA, cluster barrier, row value (warp 0) -> s_st
     auto exchange = [&](int phase) {
@@ -234,13 +236,22 @@ cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = dyn;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: this grid may be scheduled while the previous kernel on
+    // the stream runs (it waits for its completion before touching memory): the launch latency
+    // of back-to-back short calls overlaps (development override TP_PDL=0)
+    static const int pdl = [] {
+        const char* e = getenv("TP_PDL");
+        return e ? atoi(e) : 1;
+    }();
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, a, CL);
 }
 
