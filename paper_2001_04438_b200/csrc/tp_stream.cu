@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
     __shared__ __align__(8) uint64_t pempty_bar[R];
     __shared__ unsigned s_epoch;
 
+    pdl_wait_and_release();  // programmatic launch: the previous grid on the stream is complete
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     In* stages = reinterpret_cast<In*>(dsm);
@@ -489,8 +490,23 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     // queue chunks and the part-slot backlog; measured: C4 gains up to L ~ 50 rows)
     a.L = lookahead_rows(a, grid, S + 12, o);
     last_plan() = Plan{2, A, grid, 0, a.L, a.hold};
-    kern<<<(unsigned)grid, kStreamThreads, dyn, s>>>(a);
-    return cudaGetLastError();
+    // programmatic dependent launch (the kernel waits for the previous grid before touching
+    // memory): the launch overlaps the previous kernel's tail (development override TP_PDL=0)
+    static const int pdl = [] {
+        const char* e = getenv("TP_PDL");
+        return e ? atoi(e) : 1;
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kStreamThreads);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 #define TP_INSTANTIATE(IN)                                                                     \
