@@ -26,7 +26,10 @@
  *              overlap of x and y is rejected.  bf16 entry points reject overlap.
  *   Streams    Enqueue-only: the call returns after launching on `stream`
  *              (0 = legacy default stream) without synchronising.  Execution
- *              errors surface at the caller's next synchronisation.
+ *              errors surface at the caller's next synchronisation.  Some kernels
+ *              are programmatic dependent launches: they may be scheduled while
+ *              the stream's previous kernel runs but touch no memory before it
+ *              has completed, so stream order is kept.
  *   Workspace  Entry points without a workspace argument use one internal
  *              per-device workspace (allocated, zero-filled and grown on first
  *              use; growth synchronises the device).  Calls that use it must not
