@@ -107,7 +107,7 @@ __device__ __forceinline__ Item decode_item(int64_t item64, int64_t R64, int64_t
     }
     const uint32_t s = lo;
     const uint32_t pmax = (uint32_t)(P - 1);
-    const int p_hi = (int)(s / L < pmax ? s / L : pmax);
+    const int p_hi = (int)min(s / L, pmax);
     const uint32_t idx = unit - units_before(s, R, L, P);
     it.phase = p_hi - (int)idx;  // within a slot: oldest row (highest phase) first
     it.row = s - (uint32_t)it.phase * L;
