@@ -149,6 +149,9 @@ __device__ __forceinline__ Pair pass1_thread(const BlockVals& r, int valid, int 
     AccV acc = accv_init();
 #pragma unroll
     for (int g = 0; g < kPerThread / 8; ++g) {
+        // a partial block: this thread's later elements are all masked (element offsets grow
+        // with the index), and a masked group adds exactly nothing: stop (short rows, tails)
+        if (!FULL && !(elem_off<V>(8 * g, tid) < valid)) break;
         float2 m[4], v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -197,12 +200,15 @@ __device__ __forceinline__ float2 pass2_pair(float2 x, const Pass2Consts& k) {
     return fmul2(p, s);
 }
 
-// In place on this thread's values.
-template <bool CLAMP>
-__device__ __forceinline__ void pass2_thread(BlockVals& r, float nsum1, float lam_half) {
+// In place on this thread's values (those at element offsets >= valid are left as they are:
+// the caller stores only valid elements).
+template <bool CLAMP, int V = 4>
+__device__ __forceinline__ void pass2_thread(BlockVals& r, float nsum1, float lam_half, int valid = kBlockElems,
+                                             int tid = (int)threadIdx.x) {
     const Pass2Consts k = pass2_consts(nsum1, lam_half);
 #pragma unroll
     for (int i = 0; i < kPerThread; i += 2) {
+        if (valid < kBlockElems && !(elem_off<V>(i, tid) < valid)) break;
         const float2 y = pass2_pair<CLAMP>(make_float2(r.v[i], r.v[i + 1]), k);
         r.v[i] = y.x;
         r.v[i + 1] = y.y;
@@ -317,8 +323,10 @@ template <int V, bool FULL>
 __device__ __forceinline__ float max_thread(const BlockVals& r, int valid) {
     float mx = -__int_as_float(0x7f800000);
 #pragma unroll
-    for (int i = 0; i < kPerThread; ++i)
-        if (FULL || elem_off<V>(i) < valid) mx = fmaxf(mx, r.v[i]);
+    for (int i = 0; i < kPerThread; ++i) {
+        if (!FULL && !(elem_off<V>(i) < valid)) break;  // later elements are all masked
+        mx = fmaxf(mx, r.v[i]);
+    }
     return mx;
 }
 
@@ -329,6 +337,7 @@ __device__ __forceinline__ float exp_sum_thread(BlockVals& r, int valid, float m
     float2 s = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int i = 0; i < kPerThread; i += 2) {
+        if (!FULL && !(elem_off<V>(i) < valid)) break;  // later elements masked: + 0 exactly
         float2 e = exp_flush2(fadd2(make_float2(r.v[i], r.v[i + 1]), bc2(-mu)));
         if (!FULL) {
             if (!(elem_off<V>(i) < valid)) e.x = 0.0f;

@@ -35,8 +35,8 @@ __device__ __forceinline__ void op_pass2(BlockVals& r, float4 st, bool clamp, fl
         else pass2_store_full<V, false>(r, st.x, st.y, yb, tid);
         return;
     }
-    if (clamp) pass2_thread<true>(r, st.x, st.y);
-    else pass2_thread<false>(r, st.x, st.y);
+    if (clamp) pass2_thread<true, V>(r, st.x, st.y, valid, tid);
+    else pass2_thread<false, V>(r, st.x, st.y, valid, tid);
     store_block<V>(yb, valid, vec, r, tid);
 }
 
@@ -65,7 +65,8 @@ __device__ __forceinline__ void op_expsum(BlockVals& r, int valid, float mu, Par
 
 template <int V>
 __device__ __forceinline__ void op_out_recompute(BlockVals& r, float4 st, float* yb, int valid, bool vec) {
-    exp_sum_thread<V, false>(r, valid, st.x);
+    if (valid == kBlockElems) exp_sum_thread<V, true>(r, valid, st.x);
+    else exp_sum_thread<V, false>(r, valid, st.x);
     scale_thread(r, st.y);  // Y_i <- lambda * Exp(X_i - mu)
     store_block<V>(yb, valid, vec, r);
 }
