@@ -161,9 +161,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     __shared__ ClCmd cmds[2][C];                          // team A (pass 1) / team B (pass 2) queues
     __shared__ __align__(16) Pair tpairs[T][kThreads];     // thread pairs of pass-1 blocks
     __shared__ unsigned char cbits[T][kWarps];            // per-warp clamp decisions of those blocks
-    __shared__ unsigned lmask[2][kClMaxLocal];            // per-block clamp masks, by row parity
     __shared__ __align__(16) float2 rowvals[2][kClMaxNb];  // written by every CTA of the cluster
-    __shared__ float2 row_st[2];                          // (n_sum - 1, 0.5 / m_sum) of a row
+    __shared__ float4 row_st[2];                          // (n_sum - 1, 0.5 / m_sum, any local block clamped)
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
     __shared__ __align__(8) uint64_t cfull_bar[2][C];
@@ -346,6 +345,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         long long p = 0;
         for (int k = 0; k < K; ++k) {
             const int par = k & 1;
+            const int64_t row = cid + (int64_t)k * ncl;
             int b_lo, nloc;
             cl_share(nb, CL, (q + k) % CL, &b_lo, &nloc);
             float2 lval = make_float2(0.f, 0.f);  // lane li: value of local block li
@@ -369,8 +369,13 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 }
             }
             if (!ok) break;
+            // the local blocks' clamp masks for team B's pass 2, in the workspace by (row, block):
+            // a shared slot per row parity could be rewritten two rows later while team B still
+            // reads it (team B can trail the tree warp by more than a row when shares are short)
+            unsigned* block_clamp = reinterpret_cast<unsigned*>(a.ws + a.lay.block_clamp);
+            const bool anyc = __any_sync(0xffffffffu, lane < nloc && lm != 0u);
             if (lane < nloc) {
-                lmask[par][lane] = lm;
+                if (anyc) block_clamp[row * nb + b_lo + lane] = lm;  // all local blocks of a flagged row
                 const uint32_t dst = smem_u32(&rowvals[par][b_lo + lane]);
                 for (int r = 0; r < CL; ++r) st_cluster_f2(mapa(dst, (uint32_t)r), lval);
             }
@@ -380,7 +385,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             if (!wait_cluster_or_abort(&row_bar[par], (uint32_t)((k >> 1) & 1), err, 256u)) break;
             const float2 st = cl_row_stats(rowvals[par], nb);
             if (lane == 0) {
-                row_st[par] = st;
+                if (anyc) __threadfence_block();  // the block_clamp stores (all lanes) before the flag
+                row_st[par] = make_float4(st.x, st.y, anyc ? 1.0f : 0.0f, 0.0f);
                 mbar_arrive(&st_bar[par]);
             }
         }
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     // the canonical layout, so every rounding is that of the 16-warp kernels.
     const bool teamB = warp >= kClTeam;
     const int pw = teamB ? warp - kClTeam : warp;
-    float2 st = make_float2(0.f, 0.f);
+    float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
     long long np1 = 0;  // pass-1 blocks handed to the tree warp (team A)
     unsigned long long pc[kProfComputeTotal] = {0, 0, 0, 0, 0};
     const unsigned long long pc_start = PROF ? clock64() : 0ull;
@@ -454,7 +460,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 st = row_st[par];
                 lap(kProfRowWait);
             }
-            const unsigned mask = lmask[par][cmd.flags >> 8];
+            const unsigned mask = st.z != 0.0f   // some local block of the row took the clamped path
+                ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) + row * a.nb + blk) : 0u;
             float* yb = a.y + row * a.cols + (int64_t)blk * kBlockElems;
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {

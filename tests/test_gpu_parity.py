@@ -559,3 +559,21 @@ def test_three_pass_cluster_schedule_agrees_bitwise(rows, cols, dtype):
         assert tp.watchdog_flags() == 0
         if rows * cols <= 8_000_000:
             assert_parity(x, ref, f"{algo} cluster")
+
+
+@pytest.mark.parametrize("cl", [1, 2, 4])
+def test_cluster_clamp_masks_with_short_shares(cl):
+    # regression (found by tools/soak.py): with 1-2 blocks per CTA per row, team B of the cluster
+    # kernel could trail the tree warp by two rows and read a later row's clamp masks from a
+    # per-parity shared slot; masks now travel through the workspace by (row, block)
+    rows, cols = 93, 74316
+    x = workloads.ragged_case(rows, cols, -400.0, 400.0, seed=36, stream=7)
+    for r in range(0, rows, 5):  # out-of-domain elements in many rows, blocks and warps
+        x[r, (r * 7919 + 62136) % cols] = 3.0e7
+    xd = to_dev(x)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    for _ in range(3):
+        y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_CLUSTER, cluster_size=cl))
+        assert tp.last_plan()["kernel"] == "cluster"
+        assert np.array_equal(ref, y)
+    assert tp.watchdog_flags() == 0
