@@ -26,6 +26,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--minutes", type=float, default=10.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--clamp-frac", type=float, default=0.1)
+    ap.add_argument("--bf16-frac", type=float, default=0.3)
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     t_end = time.time() + 60 * args.minutes
@@ -34,24 +36,40 @@ def main():
         nb = int(rng.choice([1, 2, 3, 5, 17, 49, 64, 65, 130, 300]))
         cols = max(1, nb * 16384 - int(rng.integers(0, 16384)))
         rows = int(rng.integers(1, max(2, min(300, (64 << 20) // (cols * 4)))))
-        dtype = "bf16" if rng.random() < 0.3 else "f32"
+        dtype = "bf16" if rng.random() < args.bf16_frac else "f32"
         algo = int(rng.choice([tp.ALGO_TWO_PASS, tp.ALGO_RECOMPUTE, tp.ALGO_RELOAD]))
         sched = int(rng.choice(SCHEDS))
         cl = int(rng.choice([0, 1, 2, 4, 8]))
         grid = int(rng.choice([0, 0, 0, 7, 33]))
         x = workloads.ragged_case(rows, cols, -400.0, 400.0, seed=n, stream=7)
-        if rng.random() < 0.1:
-            x[0, int(rng.integers(0, cols))] = 3.0e7  # out of domain: the clamped path
+        if rng.random() < args.clamp_frac:  # out of domain: the clamped path, in a few rows
+            for r in rng.integers(0, rows, 1 + rows // 8):
+                x[int(r), int(rng.integers(0, cols))] = 3.0e7
         if dtype == "bf16":
             x = workloads.to_bf16(x)
             xd = torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16)
         else:
             xd = torch.from_numpy(x).cuda()
         ref = tp.softmax_ex(xd, algo, schedule=tp.SCHED_STREAM)
+        if algo == tp.ALGO_TWO_PASS and rng.random() < 0.15:  # the split path: partial / finish
+            W = int(rng.choice([1, 2, 4]))
+            per = -(-(-(-cols // 16384)) // W) * 16384  # block-aligned chunk width
+            chunks = [xd[:, w * per:min(cols, (w + 1) * per)].contiguous() for w in range(W)]
+            chunks = [c for c in chunks if c.shape[1]]
+            pairs = torch.stack([tp.partial(c) for c in chunks])
+            y = torch.cat([tp.finish(c, pairs, len(chunks)) for c in chunks], dim=1)
+            plan = {"split": len(chunks)}
+            same = bool(torch.equal(y, ref))
+            if not same and (len(chunks) & (len(chunks) - 1)) == 0 and cols % (16384 * len(chunks)) == 0:
+                bad += 1
+                print(json.dumps({"bad_split": [rows, cols, dtype, W]}), flush=True)
+            n += 1
+            del x, xd, ref, y
+            continue
         y = tp.softmax_ex(xd, algo, schedule=sched, cluster_size=cl, grid_ctas=grid)
         plan = tp.last_plan()
         ok = bool(torch.equal(y, ref)) and tp.watchdog_flags() == 0
-        if ok and rows * cols <= 2_000_000 and (x != 3.0e7).all():
+        if ok and rows * cols <= 2_000_000 and not (x == 3.0e7).any():
             try:
                 assert_parity(x, y.cpu().numpy(), "soak")
             except AssertionError:
