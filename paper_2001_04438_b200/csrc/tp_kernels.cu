@@ -291,7 +291,11 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
                 const cudaError_t e = launch_split<In>(a, CL, tail, tail_ctas, tail_cl, o, s);
                 if (e != cudaErrorNotSupported) return e;
             }
-            if (CL) return launch_rowcl<In>(a, CL, o, s);
+            if (CL) {
+                const cudaError_t e = launch_rowcl<In>(a, CL, o, s);
+                if (e != cudaErrorNotSupported) return e;
+                cudaGetLastError();
+            }
         }
         // the Three-Pass comparators on a one-cluster-per-row schedule (tp_rowcl3.cu; opt-in:
         // faster than their stream schedule for some algorithm / dtype pairs on C4, slower for

@@ -34,6 +34,11 @@ namespace tp {
 
 constexpr int kClMaxNb = 256;            // blocks per row (rows of up to 4 Mi elements)
 constexpr int kClMaxLocal = 32;          // blocks per CTA per row (lane of warp 0 per block)
+// Fewest blocks per CTA per row: more than the pass-2 pool holds (1.5 blocks fp32, 3 bf16), so
+// that producer B cannot finish pushing a row's commands (and let producer A, then the tree warp,
+// run two rows ahead) before team B has waited for that row's statistics: the tree warp can
+// then never complete a parity slot's barrier twice ahead of team B.
+template <typename In> constexpr int kClMinLocal = sizeof(In) == 4 ? 2 : 4;
 constexpr int kClThreads = kThreads + 96;  // + producer A, tree warp, producer B
 constexpr int kClCmdSlots = 16;
 constexpr int kClTeam = kWarps / 2;     // warps per compute team
@@ -558,7 +563,7 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
     int best = 0;
     double best_t = 0.0;
     for (int CL = 1; CL <= 16; CL *= 2) {
-        if (CL > nb || (nb + CL - 1) / CL > kClMaxLocal) continue;
+        if (CL > nb || (nb + CL - 1) / CL > kClMaxLocal || nb / CL < kClMinLocal<In>) continue;
         if (force_cl && CL != force_cl) continue;
         const int Q = max_active_clusters<In>(dev, CL, dyn);
         if (Q < 1) continue;
@@ -588,7 +593,8 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
         if ((env_split || (!force_cl && vs_stream)) && full > 0 && idle >= 8) {
             int cls = 1;
             while ((nb + cls - 1) / cls > kClMaxLocal) cls *= 2;
-            if (cls > 2 || max_active_clusters<In>(dev, cls, dyn) < 1) cls = 0;  // stream side launch
+            // stream-kernel side launch when pairs do not fit, or shares would be too short
+            if (cls > 2 || nb / cls < kClMinLocal<In> || max_active_clusters<In>(dev, cls, dyn) < 1) cls = 0;
             const int64_t qs = cls ? idle / cls : idle;
             // at most one round of the clusters moves to the side launch (more measured slower:
             // the side rows' L2 footprint and DRAM traffic slow the clusters down)
@@ -631,6 +637,8 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
 
 template <typename In>
 cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
+    if (CL < 1 || CL > a.nb || a.nb / CL < kClMinLocal<In> || (a.nb + CL - 1) / CL > kClMaxLocal)
+        return cudaErrorNotSupported;
     int dev = 0;
     cudaGetDevice(&dev);
     rowcl_configure<In>(dev);
