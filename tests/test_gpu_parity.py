@@ -384,13 +384,16 @@ def test_host_pipeline_matches_device_path(key):
 
 
 def test_host_pipeline_slab_ramp_bitwise():
-    # 100 rows of C4 (320 MB): a doubling ramp of small slabs at both ends, full slabs between,
-    # alternating streams; every slab's launch gives the device path's bits
-    x = workloads.generate("c4", 0, 100)
-    hx = torch.from_numpy(x).pin_memory()
+    # 200 rows of C4 bf16 (320 MB in): a doubling ramp of small slabs at both ends, full slabs
+    # between, alternating streams; every slab's launch gives the device path's bits (fp32 too)
+    x = workloads.generate("c4b", 0, 200)
+    hx = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
     hy = tp.softmax_host(hx)
-    ref = to_host(tp.softmax(to_dev(x)))
+    ref = to_host(tp.softmax(hx.cuda()))
     assert np.array_equal(hy.numpy(), ref)
+    x = workloads.generate("c4", 0, 100)
+    hy = tp.softmax_host(torch.from_numpy(x).pin_memory())
+    assert np.array_equal(hy.numpy(), to_host(tp.softmax(to_dev(x))))
 
 
 def test_host_pipeline_bf16_and_multi_slab():
