@@ -583,3 +583,14 @@ def test_cluster_clamp_masks_with_short_shares(cl):
     assert tp.watchdog_flags() == 0
     y4 = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_CLUSTER, cluster_size=4))
     assert tp.last_plan()["kernel"] == "stream" and np.array_equal(ref, y4)
+
+
+def test_randomised_soak_short():
+    # tools/soak.py for 20 s (random shapes, dtypes, algorithms, schedules, grids, out-of-domain
+    # values, the partial / finish split): every output bitwise equal to the stream schedule's
+    import subprocess
+    import sys
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "tools/soak.py", "--minutes", "0.33", "--seed", "11", "--clamp-frac", "0.3"],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
