@@ -66,6 +66,15 @@ def main():
             n += 1
             del x, xd, ref, y
             continue
+        if algo == tp.ALGO_TWO_PASS and rng.random() < 0.05:  # the host-buffer pipeline
+            hx = xd.cpu().pin_memory()
+            hy = tp.softmax_host(hx)
+            if not torch.equal(hy, tp.softmax_ex(xd, algo).cpu()):
+                bad += 1
+                print(json.dumps({"bad_host": [rows, cols, dtype]}), flush=True)
+            n += 1
+            del x, xd, ref, hx, hy
+            continue
         y = tp.softmax_ex(xd, algo, schedule=sched, cluster_size=cl, grid_ctas=grid)
         plan = tp.last_plan()
         ok = bool(torch.equal(y, ref)) and tp.watchdog_flags() == 0
