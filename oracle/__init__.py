@@ -18,7 +18,9 @@ Contents
       and exact rational arithmetic of (m, n) pairs.
 
 Every function is pinned in tests/test_oracle_pins.py (closed forms,
-invariants, mpmath brute force, two-formula agreement).  No parity is
+invariants, mpmath brute force, two-formula agreement); exp_scaled and the
+rounding of ExtExp's n (both oracle versions) against mpmath at 50 digits over
+|x| <= 2^21, next to half-integer products included.  No parity is
 unpinned in this package; the one unpinned item of the build (the paper's
 exact polynomial coefficients) is not computed here at all.
 """

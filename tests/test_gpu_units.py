@@ -148,9 +148,7 @@ def test_exp_with_reconstruction_ulp():
 
 # ------------------------------------------------------------------ exhaustive-lite ULP metrology (NEXT-2)
 
-def _ulp32(v):
-    v = np.asarray(v, np.float64)
-    return np.exp2(np.floor(np.log2(v)) - 23)
+from ulp import ulp32 as _ulp32  # noqa: E402  (pinned at binade edges in test_oracle_pins.py)
 
 
 @pytest.mark.parametrize("what", ["exp", "extexp"])
