@@ -47,7 +47,12 @@
  *   Status     0 TP_OK; 1 TP_EINVAL (null pointer, rows < 1 or cols < 1, partial
  *              x/y overlap, world < 1, workspace too small); 2 TP_ECUDA (launch
  *              or allocation error: see softmax_last_cuda_error()); 3 TP_ENODEV
- *              (no CUDA device).  Nothing is launched when the status is not 0.
+ *              (no CUDA device); 4 TP_EWATCHDOG (an EARLIER launch on this device
+ *              gave up a wait after 4 s, or a mailbox wait timed out, and its
+ *              outputs are invalid: reported once, by the first call after the
+ *              abort became visible to the host; the library has reset its state
+ *              and the next call runs normally).  Nothing is launched when the
+ *              status is not 0.
  */
 #ifndef TWOPASS_H
 #define TWOPASS_H
@@ -60,7 +65,7 @@
 extern "C" {
 #endif
 
-enum { TP_OK = 0, TP_EINVAL = 1, TP_ECUDA = 2, TP_ENODEV = 3 };
+enum { TP_OK = 0, TP_EINVAL = 1, TP_ECUDA = 2, TP_ENODEV = 3, TP_EWATCHDOG = 4 };
 
 /* Algorithm and input-dtype selectors of the _ex entry points. */
 enum { TP_ALGO_TWO_PASS = 0, TP_ALGO_THREE_PASS_RECOMPUTE = 2, TP_ALGO_THREE_PASS_RELOAD = 3 };
@@ -94,11 +99,39 @@ int softmax_f32_finish(const float* x, float* y, int64_t rows, int64_t cols, con
 int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t cols, const float* pairs,
                             int world, cudaStream_t stream);
 
+/* ---- Three-Pass comparators for sharded rows (multi-GPU Alg. 1 / Alg. 2) ----
+ * The comparators need TWO exchanges per call where the Two-Pass needs one:
+ *   max_partial : pass 1 over the local chunk -> max_out[r] (device, rows fp32)
+ *   -> gather every rank's maxima: maxes, device, world x rows, rank-major
+ *   sum_partial : mu = max over ranks; pass 2 (PAPER.md:93-95 / 111-117) over the local chunk ->
+ *                 sum_out[r] = sum of Exp(x - mu) (device, rows); Reload (algo 3) also writes
+ *                 y = Exp(x - mu) (y may be NULL for Recompute)
+ *   -> gather every rank's sums: sums, device, world x rows, rank-major
+ *   finish      : sigma = canonical tree over rank index of the sums (reading G8), lambda =
+ *                 1/sigma; pass 3 (PAPER.md:96-98 / 119-121): y = lambda Exp(x - mu) (Recompute,
+ *                 re-reads x) or y = lambda y (Reload, re-reads y)
+ * algo: TP_ALGO_THREE_PASS_RECOMPUTE or TP_ALGO_THREE_PASS_RELOAD (the same for all three calls).
+ * With world == 1 (maxes / sums = the chunk's own results) the outputs equal softmax3_*'s bit for
+ * bit; with a power-of-two world and equal chunks that are power-of-two runs of 16384-element
+ * blocks, bitwise those of one GPU.  Workspace as for softmax_ex (NULL, 0 = internal; one per
+ * concurrent stream).  Asynchronous; statuses as above. */
+int softmax3_max_partial_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, float* max_out, void* workspace,
+                            size_t workspace_bytes, cudaStream_t stream);
+int softmax3_sum_partial_ex(int algo, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols,
+                            const float* maxes, int world, float* sum_out, void* workspace, size_t workspace_bytes,
+                            cudaStream_t stream);
+int softmax3_finish_ex(int algo, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* maxes,
+                       const float* sums, int world, void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
 /* ---- one-sided pair exchange over NVLink (rank merge without a collective) --
  * A mailbox (device memory of tp_mailbox_bytes(world, rows) bytes, owned by its rank, ZERO-
- * FILLED once before first use) holds: bytes [0, 4*world) one uint32 flag per rank, bytes
- * [240, 244) an error word (bit r: waiting for rank r timed out), and from byte 256 the pairs
- * float[world][rows][2] (rank-major, the layout softmax_f32_finish takes).  world <= 56.
+ * FILLED once before first use) is double-buffered by epoch parity h = epoch & 1: bytes
+ * [256 h, 256 h + 4 world) one uint32 flag per rank, bytes [512, 516) an error word (bit r:
+ * waiting for rank r timed out), and from byte tp_mailbox_pairs_offset(world, rows, epoch)
+ * (= 1024 + h * 8 * world * rows) the pairs float[world][rows][2] of that epoch (rank-major,
+ * the layout softmax_f32_finish takes).  world <= 56.  Two halves make reuse safe: a rank
+ * pushes epoch e + 2 only after its finish of e + 1, which waited for every rank's push of
+ * e + 1, issued by each rank after its own finish of e had read half e & 1.
  * tp_pairs_push: after softmax_*_partial on rank `rank`, stores its rows pairs (device) into
  *   slot `rank` of every mailbox listed in peer_mailboxes (DEVICE array of world pointers,
  *   entry p = rank p's mailbox mapped into this process: the local one, or one opened with
@@ -106,9 +139,11 @@ int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t c
  * tp_pairs_wait: on the local mailbox, waits until every flag equals `epoch` (acquire,
  *   system scope), or timeout_ns elapsed (then sets the error word; outputs are undefined).
  * Both asynchronous on `stream`; use a new epoch (e.g. 1, 2, ...) per exchange, the same on
- * all ranks.  Then softmax_*_finish(x, y, rows, cols, mailbox + 256 bytes, world, ...).
+ * all ranks.  Then softmax_*_finish(x, y, rows, cols, mailbox + tp_mailbox_pairs_offset(...),
+ * world, ...).
  * Sequence per rank: partial -> push -> wait -> finish; no NCCL, no host synchronisation.   */
 size_t tp_mailbox_bytes(int world, int64_t rows);
+size_t tp_mailbox_pairs_offset(int world, int64_t rows, unsigned epoch); /* 0 on bad arguments */
 int tp_pairs_push(const float* pairs, int64_t rows, void* const* peer_mailboxes, int rank, int world,
                   unsigned epoch, cudaStream_t stream);
 int tp_pairs_wait(const void* mailbox, int world, unsigned epoch, uint64_t timeout_ns, cudaStream_t stream);
@@ -160,8 +195,16 @@ int softmax_ex(int algo, int in_dtype, const void* x, float* y, int64_t rows, in
                size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream);
 int softmax_partial_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, float* pair_out, void* workspace,
                        size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream);
+/* softmax_finish_ex: as softmax_f32_finish / softmax_bf16_f32_finish on a caller workspace
+ *   (NULL with 0 bytes = the internal one).  Pass the workspace the chunk's partial call used:
+ *   the partial leaves there, per block, the warps whose pass 1 ran on clamped values (reading
+ *   G11, |x| > 2^21), and the finish replays exactly those choices, so outputs are bitwise
+ *   those of one GPU for any input.  With another workspace only elements outside the accuracy
+ *   domain (|x| > 2^21) can differ.  A workspace must not be used by two launches running
+ *   concurrently. */
 int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
-                      int world, const softmax_opts* opts, cudaStream_t stream);
+                      int world, void* workspace, size_t workspace_bytes, const softmax_opts* opts,
+                      cudaStream_t stream);
 
 /* ---- fused one-sided exchange (pass 1 + rank merge a7 without a collective
  * library or extra launches; mailboxes as for tp_pairs_push / tp_pairs_wait above) ----------
@@ -171,10 +214,12 @@ int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64
  *   pointers, as tp_pairs_push) and, once all `rows` pairs are stored and fenced system-wide,
  *   release-stores `epoch` (>= 1, new per exchange) into flag `rank` of every mailbox.
  *   pair_out (device, rows x 2) also receives the pairs when not NULL.
- * softmax_finish_mailbox_ex: as softmax_finish_ex with pairs = mailbox + 256 bytes, except
+ * softmax_finish_mailbox_ex: as softmax_finish_ex with pairs = this epoch's half of the mailbox, except
  *   that the kernel itself first waits (acquire, system scope) until the world flags of the
  *   LOCAL mailbox equal `epoch`; a flag missing for timeout_ns sets its rank's bit in the
- *   mailbox error word and watchdog bit 0 (outputs then undefined; nothing hangs).
+ *   mailbox error word and watchdog bit 0 (outputs then undefined; nothing hangs; the next
+ *   call on the device returns TP_EWATCHDOG).  workspace: as softmax_finish_ex (the one
+ *   softmax_partial_push_ex used).
  * Sequence per rank: partial_push -> finish_mailbox, two launches, no NCCL, no host
  * synchronisation.  Results are bit-identical to partial -> all_gather -> finish.  The epoch is
  * a launch argument: a captured CUDA graph replays the same epoch, so a graph must be captured
@@ -185,8 +230,8 @@ int softmax_partial_push_ex(int in_dtype, const void* x, int64_t rows, int64_t c
                             int rank, int world, unsigned epoch, float* pair_out, void* workspace,
                             size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream);
 int softmax_finish_mailbox_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const void* mailbox,
-                              int world, unsigned epoch, unsigned long long timeout_ns, const softmax_opts* opts,
-                              cudaStream_t stream);
+                              int world, unsigned epoch, unsigned long long timeout_ns, void* workspace,
+                              size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream);
 
 /* ---- end-to-end call on HOST buffers ---------------------------------------
  * hx, hy: HOST pointers (pinned memory gives full PCIe bandwidth).  Copies x to
@@ -229,7 +274,12 @@ int softmax_watchdog_flags(const void* workspace, int reset);
  *        2: pair merge (a[2i], a[2i+1]) + (b[2i], b[2i+1]) -> (out0, out1)
  *        3: Exp with reconstruction, argument a <= 0 -> out0 (Alg. 4)
  *        4: the kernels' 2^k for integer k (MUFU.EX2, .ftz) -> out0
- *        5: %globaltimer (ns, uint64) into out0 viewed as uint64[count] (timeline marker) */
+ *        5: %globaltimer (ns, uint64) into out0 viewed as uint64[count] (timeline marker)
+ *        6: the kernels' ExtExp exactly as pass 1 / pass 2 run it (FFMA2, no clamp):
+ *           (out0 = m, out1 = n)
+ *        7: the kernels' integer-pipe 2^k: out0 = 2^(d - 127) for d = round(a) <= 254,
+ *           +0 for d <= 0 (the scale of Alg. 3's accumulate and pass 2, PAPER.md:161, 168,
+ *           flushed below 2^-126 per PAPER.md:252-258) */
 int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                 cudaStream_t stream);
 

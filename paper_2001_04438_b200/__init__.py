@@ -23,7 +23,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # TP_LIBRARY: development override (an alternative in-tree build of the same library)
 _SO = os.environ.get("TP_LIBRARY") or os.path.join(_PKG, "libtwopass.so")
 
-TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV = 0, 1, 2, 3
+TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV, TP_EWATCHDOG = 0, 1, 2, 3, 4
 ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3
 SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER, SCHED_SMALL = 0, 1, 2, 3, 4  # twopass.h TP_SCHED_*
 IN_F32, IN_BF16 = 0, 1
@@ -35,7 +35,8 @@ EXPORTS = [
     "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_partial_push_ex", "softmax_finish_mailbox_ex", "softmax_f32_host", "softmax_bf16_f32_host",
     "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
     "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_read_probe", "tp_phase_only", "tp_exp_sweep", "tp_exp_fit",
-    "tp_mailbox_bytes", "tp_pairs_push", "tp_pairs_wait", "tp_ipc_get_handle", "tp_ipc_open", "tp_ipc_close",
+    "softmax3_max_partial_ex", "softmax3_sum_partial_ex", "softmax3_finish_ex",
+    "tp_mailbox_bytes", "tp_mailbox_pairs_offset", "tp_pairs_push", "tp_pairs_wait", "tp_ipc_get_handle", "tp_ipc_open", "tp_ipc_close",
 ]
 
 
@@ -79,11 +80,14 @@ def lib() -> ctypes.CDLL:
         L.softmax_workspace_bytes.restype = sz
         L.softmax_ex.argtypes = [ci, ci, vp, vp, i64, i64, vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
         L.softmax_partial_ex.argtypes = [ci, vp, i64, i64, vp, vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
-        L.softmax_finish_ex.argtypes = [ci, vp, vp, i64, i64, vp, ci, ctypes.POINTER(SoftmaxOpts), vp]
+        L.softmax_finish_ex.argtypes = [ci, vp, vp, i64, i64, vp, ci, vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
         L.softmax_partial_push_ex.argtypes = [ci, vp, i64, i64, vp, ci, ci, ctypes.c_uint, vp, vp, sz,
                                               ctypes.POINTER(SoftmaxOpts), vp]
         L.softmax_finish_mailbox_ex.argtypes = [ci, vp, vp, i64, i64, vp, ci, ctypes.c_uint, ctypes.c_ulonglong,
-                                                ctypes.POINTER(SoftmaxOpts), vp]
+                                                vp, sz, ctypes.POINTER(SoftmaxOpts), vp]
+        L.softmax3_max_partial_ex.argtypes = [ci, vp, i64, i64, vp, vp, sz, vp]
+        L.softmax3_sum_partial_ex.argtypes = [ci, ci, vp, vp, i64, i64, vp, ci, vp, vp, sz, vp]
+        L.softmax3_finish_ex.argtypes = [ci, ci, vp, vp, i64, i64, vp, vp, ci, vp, sz, vp]
         L.softmax_f32_host.argtypes = [vp, vp, i64, i64]
         L.softmax_bf16_f32_host.argtypes = [vp, vp, i64, i64]
         L.softmax_status_str.argtypes = [ci]
@@ -94,6 +98,8 @@ def lib() -> ctypes.CDLL:
         L.tp_exp_fit.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_uint32, i64, ci, vp, vp, vp]
         L.tp_mailbox_bytes.argtypes = [ci, i64]
         L.tp_mailbox_bytes.restype = sz
+        L.tp_mailbox_pairs_offset.argtypes = [ci, i64, ctypes.c_uint]
+        L.tp_mailbox_pairs_offset.restype = sz
         L.tp_pairs_push.argtypes = [vp, i64, vp, ci, ci, ctypes.c_uint, vp]
         L.tp_pairs_wait.argtypes = [vp, ci, ctypes.c_uint, ctypes.c_uint64, vp]
         L.tp_ipc_get_handle.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
@@ -214,17 +220,63 @@ def partial(x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.T
     return p
 
 
+def _ws(workspace: torch.Tensor | None):
+    return (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel() * workspace.element_size())
+
+
 def finish(x: torch.Tensor, pairs: torch.Tensor, world: int, out: torch.Tensor | None = None,
-           grid_ctas: int = 0) -> torch.Tensor:
-    """Merge `world` partials per row (pairs: [world, rows, 2]) and run pass 2 on the local chunk."""
+           grid_ctas: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Merge `world` partials per row (pairs: [world, rows, 2]) and run pass 2 on the local chunk.
+    `workspace`: the one the chunk's partial() used (None: the internal one, as partial's None)."""
     x = _prep(x)
     rows, cols = _rows_cols(x)
     assert pairs.is_cuda and pairs.dtype == torch.float32 and pairs.is_contiguous()
     assert pairs.numel() == world * rows * 2
     y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
     st = lib().softmax_finish_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, pairs.data_ptr(), world,
-                                 _opts(grid_ctas), _stream(x))
+                                 *_ws(workspace), _opts(grid_ctas), _stream(x))
     _check(st, "finish")
+    return y
+
+
+# ---- sharded Three-Pass comparators (include/twopass.h softmax3_*_partial_ex / finish_ex)
+
+def softmax3_max_partial(x: torch.Tensor, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Alg. 1/2 pass 1 over a chunk of each row -> [rows] fp32 maxima."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    out = torch.empty(rows, dtype=torch.float32, device=x.device)
+    _check(lib().softmax3_max_partial_ex(_in_dtype(x), x.data_ptr(), rows, cols, out.data_ptr(), *_ws(workspace),
+                                         _stream(x)), "softmax3_max_partial")
+    return out
+
+
+def softmax3_sum_partial(x: torch.Tensor, algo: int, maxes: torch.Tensor, out: torch.Tensor | None = None,
+                         workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Pass 2 over the chunk with mu = max over the world's maxima ([world, rows]) -> [rows] sums;
+    Reload also writes exp(x - mu) into `out` (allocated if None)."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    assert maxes.is_cuda and maxes.dtype == torch.float32 and maxes.is_contiguous() and maxes.numel() % rows == 0
+    if algo == ALGO_RELOAD and out is None:
+        out = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    sums = torch.empty(rows, dtype=torch.float32, device=x.device)
+    _check(lib().softmax3_sum_partial_ex(algo, _in_dtype(x), x.data_ptr(), None if out is None else out.data_ptr(),
+                                        rows, cols, maxes.data_ptr(), maxes.numel() // rows, sums.data_ptr(),
+                                        *_ws(workspace), _stream(x)), "softmax3_sum_partial")
+    return sums
+
+
+def softmax3_finish(x: torch.Tensor, algo: int, maxes: torch.Tensor, sums: torch.Tensor,
+                    out: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Pass 3 over the chunk with mu, sigma merged from the world's partials ([world, rows] each)."""
+    x = _prep(x)
+    rows, cols = _rows_cols(x)
+    assert maxes.numel() == sums.numel() and maxes.numel() % rows == 0
+    y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
+    _check(lib().softmax3_finish_ex(algo, _in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, maxes.data_ptr(),
+                                    sums.data_ptr(), maxes.numel() // rows, *_ws(workspace), _stream(x)),
+           "softmax3_finish")
     return y
 
 
@@ -245,14 +297,15 @@ def partial_push(x: torch.Tensor, peer_ptrs: torch.Tensor, rank: int, world: int
 
 
 def finish_mailbox(x: torch.Tensor, mailbox: torch.Tensor, world: int, epoch: int, timeout_ns: int,
-                   out: torch.Tensor | None = None, grid_ctas: int = 0) -> torch.Tensor:
+                   out: torch.Tensor | None = None, grid_ctas: int = 0,
+                   workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Await `epoch` in the local mailbox inside the kernel, merge its world pairs per row, pass 2
     (softmax_finish_mailbox_ex)."""
     x = _prep(x)
     rows, cols = _rows_cols(x)
     y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
     st = lib().softmax_finish_mailbox_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, mailbox.data_ptr(),
-                                         world, epoch, timeout_ns, _opts(grid_ctas), _stream(x))
+                                         world, epoch, timeout_ns, *_ws(workspace), _opts(grid_ctas), _stream(x))
     _check(st, "finish_mailbox")
     return y
 

@@ -29,16 +29,35 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = SO, defines: tuple = ()) -> str:
+    """Compile every source to an object in parallel (build/<tag>/), then link the shared library."""
     if not force and out == SO and not _stale():
         return SO
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines], "-o", out,
-           *[os.path.join(CSRC, f) for f in SOURCES]]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    tag = "release" if not defines else "_".join(d.replace("=", "-") for d in defines)
+    odir = os.path.join(ROOT, "build", tag)
+    os.makedirs(odir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    extra = [*(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines]]
+
+    def compile_one(src):
+        obj = os.path.join(odir, src.replace(".cu", ".o"))
+        r = subprocess.run([NVCC, *cflags, *extra, "-c", "-o", obj, os.path.join(CSRC, src)],
+                           capture_output=True, text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for src, _, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed compiling {src}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    r = subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out,
+                        *[obj for _, obj, _ in results]], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libtwopass.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libtwopass.so")
     return out
 
 

@@ -83,6 +83,42 @@ void forget_ws(const void* ws) {
     g_ws_shape.erase(ws);
 }
 
+// ---- watchdog aborts (include/twopass.h TP_EWATCHDOG).  A launch that gives up on a wait
+// stores 1 into its device's word of this host-mapped array (tp_sched.cuh raise_abort); the
+// next call on that device sees it, clears it, forgets every workspace's shape (so every
+// control region, the header's error word included, is re-zeroed before its next launch) and
+// returns TP_EWATCHDOG without launching anything.
+std::once_flag g_abort_once;
+unsigned* g_abort_host = nullptr;   // kMaxDev words, host view
+unsigned* g_abort_dev = nullptr;    // the same words, device view
+
+void abort_init() {
+    std::call_once(g_abort_once, [] {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, sizeof(unsigned) * kMaxDev, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return;  // no abort reporting (the workspace flags still record aborts)
+        }
+        memset(p, 0, sizeof(unsigned) * kMaxDev);
+        void* d = nullptr;
+        if (cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess) {
+            cudaGetLastError();
+            d = p;  // unified addressing: the host pointer is valid on the device
+        }
+        g_abort_host = static_cast<unsigned*>(p);
+        g_abort_dev = static_cast<unsigned*>(d);
+    });
+}
+
+bool take_abort(int dev) {
+    abort_init();
+    if (!g_abort_host || !__atomic_load_n(&g_abort_host[dev], __ATOMIC_ACQUIRE)) return false;
+    __atomic_store_n(&g_abort_host[dev], 0u, __ATOMIC_RELEASE);
+    std::lock_guard<std::mutex> lk(g_shape_mu);
+    g_ws_shape.clear();
+    return true;
+}
+
 // Grow-only zero-filled device buffer.  Growth synchronises the device (documented).
 int ensure_zeroed(void** p, size_t* have, size_t need) {
     if (*have >= need && *p) return TP_OK;
@@ -132,6 +168,7 @@ int check_args(int in_dtype, const void* x, const float* y, int64_t rows, int64_
         if (overlap_bad(x, (size_t)(rows * cols) * esz, y, (size_t)(rows * cols) * 4, in_dtype == TP_IN_F32))
             return TP_EINVAL;
     }
+    if (take_abort(dev)) return TP_EWATCHDOG;  // an earlier launch on this device gave up
     return TP_OK;
 }
 
@@ -186,14 +223,24 @@ int run_partial(int in_dtype, const void* x, int64_t rows, int64_t cols, float* 
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 
+// A workspace argument (or the internal one for NULL), checked and prepared for (rows, cols).
+int workspace_for(void** ws, size_t ws_bytes, int64_t rows, int64_t cols, cudaStream_t s) {
+    const size_t need = tp::workspace_bytes(rows, cols);
+    int st;
+    if (*ws) {
+        if (ws_bytes < need) return TP_EINVAL;
+    } else if ((st = internal_workspace(need, ws))) {
+        return st;
+    }
+    return prepare_ws(*ws, rows, cols, s);
+}
+
 int run_finish(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs, int world,
-               const softmax_opts* opts, cudaStream_t s) {
+               void* ws, size_t ws_bytes, const softmax_opts* opts, cudaStream_t s) {
     int st = check_args(in_dtype, x, y, rows, cols, true);
     if (st) return st;
-    if (!pairs || world < 1) return TP_EINVAL;
-    void* ws = nullptr;
-    if ((st = internal_workspace(tp::workspace_bytes(rows, cols), &ws))) return st;
-    if ((st = prepare_ws(ws, rows, cols, s))) return st;
+    if (!pairs || world < 1 || (!ws && ws_bytes)) return TP_EINVAL;
+    if ((st = workspace_for(&ws, ws_bytes, rows, cols, s))) return st;
     cudaError_t e = tp::launch_finish(in_dtype == TP_IN_BF16, x, y, rows, cols, pairs, world, ws, to_opts(opts), s);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
@@ -234,7 +281,10 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         const int64_t cl = cols / K;
         if ((st = ensure_zeroed(&d.row_x, &d.row_x_bytes, (size_t)n * esz))) return st;
         if ((st = ensure_zeroed(&d.row_y, &d.row_y_bytes, (size_t)n * 4))) return st;
-        if ((st = ensure_zeroed(&d.row_ws, &d.row_ws_bytes, tp::workspace_bytes(1, cl)))) return st;
+        // one workspace per chunk: a chunk's finish reads the per-block clamp decisions its
+        // partial left there (reading G11)
+        const size_t wstride = (tp::workspace_bytes(1, cl) + 255) & ~size_t(255);
+        if ((st = ensure_zeroed(&d.row_ws, &d.row_ws_bytes, wstride * K))) return st;
         if ((st = ensure_zeroed(&d.pairs, &d.pairs_bytes, sizeof(float) * 2 * K))) return st;
         char* dx = (char*)d.row_x;
         float* dy = (float*)d.row_y;
@@ -247,14 +297,15 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
             if (e != cudaSuccess) return cuda_fail(e);
             cudaEventRecord(d.ev[c], cp);
             cudaStreamWaitEvent(cm, d.ev[c], 0);
-            if ((st = prepare_ws(d.row_ws, 1, cl, cm))) return st;
-            e = tp::launch_partial(in_dtype == TP_IN_BF16, dx + (size_t)c * cl * esz, 1, cl, pairs + 2 * c,
-                                   d.row_ws, lo, cm);
+            void* wsc = (char*)d.row_ws + wstride * c;
+            if ((st = prepare_ws(wsc, 1, cl, cm))) return st;
+            e = tp::launch_partial(in_dtype == TP_IN_BF16, dx + (size_t)c * cl * esz, 1, cl, pairs + 2 * c, wsc, lo,
+                                   cm);
             if (e != cudaSuccess) return cuda_fail(e);
         }
         for (int c = 0; c < K; ++c) {  // pass 2 of chunk c || D2H chunk c-1
             e = tp::launch_finish(in_dtype == TP_IN_BF16, dx + (size_t)c * cl * esz, dy + (size_t)c * cl, 1, cl,
-                                  pairs, K, d.row_ws, lo, cm);
+                                  pairs, K, (char*)d.row_ws + wstride * c, lo, cm);
             if (e != cudaSuccess) return cuda_fail(e);
             cudaEventRecord(d.ev[32 + c], cm);
             cudaStreamWaitEvent(cp, d.ev[32 + c], 0);
@@ -268,21 +319,17 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
     // Row slabs of ~64 MB round-robin over 2 streams: the H2D copy of the next slab, the kernel
     // and the D2H copy of the previous slab overlap (the two copy directions run concurrently,
     // so the pipeline approaches the bidirectional PCIe rate).
-    static const size_t slab_bytes = [] {  // development override TP_HOST_SLAB_MB
-        const char* e = getenv("TP_HOST_SLAB_MB");
-        return e ? (size_t)atoi(e) << 20 : kHostSlabBytes;
-    }();
+    static const size_t slab_bytes = (size_t)tp::dev_env_int("TP_HOST_SLAB_MB", (int)(kHostSlabBytes >> 20)) << 20;
     static const int nstreams = [] {  // development override TP_HOST_STREAMS (1..kHostStreams)
-        const char* e = getenv("TP_HOST_STREAMS");
-        const int v = e ? atoi(e) : 2;
+        const int v = tp::dev_env_int("TP_HOST_STREAMS", 2);
         return v < 1 ? 1 : (v > kHostStreams ? kHostStreams : v);
     }();
     int64_t slab = (int64_t)(slab_bytes / ((size_t)cols * esz));
     if (slab < 1) slab = 1;
     if (slab > rows) slab = rows;
     const size_t need_x = (size_t)(slab * cols) * esz, need_y = (size_t)(slab * cols) * 4;
-    if (d.stage_bytes_x < need_x || d.stage_bytes_y < need_y || !d.hx_dev[kHostStreams - 1] ||
-        !d.hy_dev[kHostStreams - 1]) {
+    if (d.stage_bytes_x < need_x || d.stage_bytes_y < need_y || !d.hx_dev[nstreams - 1] ||
+        !d.hy_dev[nstreams - 1]) {
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e);
         for (int i = 0; i < kHostStreams; ++i) {
@@ -293,7 +340,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         }
         const size_t bx = need_x > d.stage_bytes_x ? need_x : d.stage_bytes_x;
         const size_t by = need_y > d.stage_bytes_y ? need_y : d.stage_bytes_y;
-        for (int i = 0; i < kHostStreams; ++i) {
+        for (int i = 0; i < nstreams; ++i) {  // one staging slot per stream in use
             if ((e = cudaMalloc(&d.hx_dev[i], bx)) != cudaSuccess) return cuda_fail(e);
             if ((e = cudaMalloc((void**)&d.hy_dev[i], by)) != cudaSuccess) return cuda_fail(e);
         }
@@ -304,14 +351,16 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
     const bool needs_ws = tp::softmax_needs_workspace(TP_ALGO_TWO_PASS, cols, lo);
     if (needs_ws) {
         const size_t wsb = tp::workspace_bytes(slab, cols);
-        if (d.hws_bytes < wsb || !d.hws[kHostStreams - 1]) {
+        if (d.hws_bytes < wsb || !d.hws[nstreams - 1]) {
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return cuda_fail(e);
             for (int i = 0; i < kHostStreams; ++i) {
                 if (d.hws[i]) {
                     cudaFree(d.hws[i]);
                     forget_ws(d.hws[i]);
+                    d.hws[i] = nullptr;
                 }
+                if (i >= nstreams) continue;
                 if ((e = cudaMalloc(&d.hws[i], wsb)) != cudaSuccess) return cuda_fail(e);
                 if ((e = cudaMemset(d.hws[i], 0, wsb)) != cudaSuccess) return cuda_fail(e);
             }
@@ -320,10 +369,7 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
     }
     // Slab sizes: full slabs in the middle, a doubling ramp at both ends (slab/8, /4, /2 ...) so
     // that the first H2D copy and the last D2H copy, which nothing overlaps, are short.
-    static const int ramp = [] {  // development override TP_HOST_RAMP=0: equal slabs
-        const char* e = getenv("TP_HOST_RAMP");
-        return e ? atoi(e) : 1;
-    }();
+    static const int ramp = tp::dev_env_int("TP_HOST_RAMP", 1);  // development: 0 = equal slabs
     std::vector<int64_t> sizes;
     {
         std::vector<int64_t> up;
@@ -366,6 +412,13 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
 
 }  // namespace
 
+namespace tp {
+unsigned* abort_word_device(int dev) {
+    abort_init();
+    return g_abort_dev && dev >= 0 && dev < kMaxDev ? g_abort_dev + dev : nullptr;
+}
+}  // namespace tp
+
 // mapped pointer -> base of the IPC mapping it was opened from (tp_ipc_open / tp_ipc_close)
 std::mutex g_ipc_mu;
 std::unordered_map<void*, void*> g_ipc_base;
@@ -398,11 +451,11 @@ int softmax_bf16_partial(const uint16_t* x, int64_t rows, int64_t cols, float* p
 }
 int softmax_f32_finish(const float* x, float* y, int64_t rows, int64_t cols, const float* pairs, int world,
                        cudaStream_t stream) {
-    return run_finish(TP_IN_F32, x, y, rows, cols, pairs, world, nullptr, stream);
+    return run_finish(TP_IN_F32, x, y, rows, cols, pairs, world, nullptr, 0, nullptr, stream);
 }
 int softmax_bf16_f32_finish(const uint16_t* x, float* y, int64_t rows, int64_t cols, const float* pairs, int world,
                             cudaStream_t stream) {
-    return run_finish(TP_IN_BF16, x, y, rows, cols, pairs, world, nullptr, stream);
+    return run_finish(TP_IN_BF16, x, y, rows, cols, pairs, world, nullptr, 0, nullptr, stream);
 }
 size_t softmax_workspace_bytes(int64_t rows, int64_t cols) {
     if (rows < 1 || cols < 1) return 0;
@@ -418,8 +471,9 @@ int softmax_partial_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, 
     return run_partial(in_dtype, x, rows, cols, pair_out, workspace, workspace_bytes, opts, stream);
 }
 int softmax_finish_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* pairs,
-                      int world, const softmax_opts* opts, cudaStream_t stream) {
-    return run_finish(in_dtype, x, y, rows, cols, pairs, world, opts, stream);
+                      int world, void* workspace, size_t workspace_bytes, const softmax_opts* opts,
+                      cudaStream_t stream) {
+    return run_finish(in_dtype, x, y, rows, cols, pairs, world, workspace, workspace_bytes, opts, stream);
 }
 int softmax_partial_push_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, void* const* peer_mailboxes,
                             int rank, int world, unsigned epoch, float* pair_out, void* workspace,
@@ -446,25 +500,65 @@ int softmax_partial_push_ex(int in_dtype, const void* x, int64_t rows, int64_t c
 }
 
 int softmax_finish_mailbox_ex(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const void* mailbox,
-                              int world, unsigned epoch, unsigned long long timeout_ns, const softmax_opts* opts,
-                              cudaStream_t stream) {
+                              int world, unsigned epoch, unsigned long long timeout_ns, void* workspace,
+                              size_t workspace_bytes, const softmax_opts* opts, cudaStream_t stream) {
     int st = check_args(in_dtype, x, y, rows, cols, true);
     if (st) return st;
     if (!mailbox || world < 1 || world > tp::kMailboxMaxWorld || epoch == 0 ||
-        (reinterpret_cast<uintptr_t>(mailbox) & 15))
+        (reinterpret_cast<uintptr_t>(mailbox) & 15) || (!workspace && workspace_bytes))
         return TP_EINVAL;
-    void* ws = nullptr;
-    if ((st = internal_workspace(tp::workspace_bytes(rows, cols), &ws))) return st;
-    if ((st = prepare_ws(ws, rows, cols, stream))) return st;
+    void* ws = workspace;
+    if ((st = workspace_for(&ws, workspace_bytes, rows, cols, stream))) return st;
     tp::Exchange xc;
     xc.world = world;
     xc.epoch = epoch;
     xc.mailbox = mailbox;
     xc.wait_ns = timeout_ns;
-    const float* pairs = reinterpret_cast<const float*>(static_cast<const char*>(mailbox) + tp::kMailboxHeader);
+    const float* pairs = reinterpret_cast<const float*>(static_cast<const char*>(mailbox) +
+                                                        tp::mailbox_pairs_offset(world, rows, epoch));
     cudaError_t e = tp::launch_finish(in_dtype == TP_IN_BF16, x, y, rows, cols, pairs, world, ws, to_opts(opts),
                                       stream, &xc);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+// ---- sharded Three-Pass comparators (multi-GPU Alg. 1 / Alg. 2)
+namespace {
+int run_shard3(int algo, int phase, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols,
+               const float* maxes, const float* sums, int world, float* out, void* ws, size_t ws_bytes,
+               cudaStream_t s) {
+    const bool need_y = phase == 2 || (phase == 1 && algo == TP_ALGO_THREE_PASS_RELOAD);
+    int st = check_args(in_dtype, x, y, rows, cols, need_y);
+    if (st) return st;
+    if (algo != TP_ALGO_THREE_PASS_RECOMPUTE && algo != TP_ALGO_THREE_PASS_RELOAD) return TP_EINVAL;
+    if (world < 1 || (phase >= 1 && !maxes) || (phase == 2 && !sums) || (phase < 2 && !out) || (!ws && ws_bytes))
+        return TP_EINVAL;
+    if ((st = workspace_for(&ws, ws_bytes, rows, cols, s))) return st;
+    tp::Shard3 sh;
+    sh.maxes = phase >= 1 ? maxes : nullptr;
+    sh.sums = phase == 2 ? sums : nullptr;
+    sh.world = world;
+    sh.out = phase < 2 ? out : nullptr;
+    cudaError_t e = tp::launch_shard3(algo, in_dtype == TP_IN_BF16, phase, x, need_y ? y : nullptr, rows, cols, ws,
+                                      sh, tp::LaunchOpts{}, s);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+}  // namespace
+
+int softmax3_max_partial_ex(int in_dtype, const void* x, int64_t rows, int64_t cols, float* max_out, void* workspace,
+                            size_t workspace_bytes, cudaStream_t stream) {
+    return run_shard3(TP_ALGO_THREE_PASS_RECOMPUTE, 0, in_dtype, x, nullptr, rows, cols, nullptr, nullptr, 1, max_out,
+                      workspace, workspace_bytes, stream);
+}
+int softmax3_sum_partial_ex(int algo, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols,
+                            const float* maxes, int world, float* sum_out, void* workspace, size_t workspace_bytes,
+                            cudaStream_t stream) {
+    return run_shard3(algo, 1, in_dtype, x, y, rows, cols, maxes, nullptr, world, sum_out, workspace, workspace_bytes,
+                      stream);
+}
+int softmax3_finish_ex(int algo, int in_dtype, const void* x, float* y, int64_t rows, int64_t cols, const float* maxes,
+                       const float* sums, int world, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+    return run_shard3(algo, 2, in_dtype, x, y, rows, cols, maxes, sums, world, nullptr, workspace, workspace_bytes,
+                      stream);
 }
 
 int softmax_f32_host(const float* hx, float* hy, int64_t rows, int64_t cols) {
@@ -479,6 +573,9 @@ const char* softmax_status_str(int status) {
         case TP_EINVAL: return "invalid argument";
         case TP_ECUDA: return "CUDA error";
         case TP_ENODEV: return "no CUDA device";
+        case TP_EWATCHDOG:
+            return "watchdog abort: an earlier launch on this device gave up waiting (its outputs are invalid); "
+                   "state reset, call again";
         default: return "unknown status";
     }
 }
@@ -516,6 +613,10 @@ int softmax_watchdog_flags(const void* workspace, int reset) {
     if (cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     if (toff && cudaMemcpy(&ht, (const char*)ws + toff, sizeof(ht), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     const unsigned err = h.error | ht.error;
+    if (reset) {  // also acknowledges a pending TP_EWATCHDOG of this device
+        int dev;
+        if (!current_device(&dev) && g_abort_host) __atomic_store_n(&g_abort_host[dev], 0u, __ATOMIC_RELEASE);
+    }
     if (reset && err) {
         unsigned z = 0;
         cudaMemcpy((char*)ws + offsetof(tp::WsHeader, error), &z, sizeof(z), cudaMemcpyHostToDevice);
@@ -591,6 +692,9 @@ int tp_exp_fit(const float* coeffs, uint32_t bits0, int64_t count, int stride, u
 
 size_t tp_mailbox_bytes(int world, int64_t rows) {
     return (world < 1 || world > tp::kMailboxMaxWorld || rows < 0) ? 0 : tp::mailbox_bytes(world, rows);
+}
+size_t tp_mailbox_pairs_offset(int world, int64_t rows, unsigned epoch) {
+    return (world < 1 || world > tp::kMailboxMaxWorld || rows < 0) ? 0 : tp::mailbox_pairs_offset(world, rows, epoch);
 }
 
 int tp_pairs_push(const float* pairs, int64_t rows, void* const* peer_mailboxes, int rank, int world,
@@ -670,8 +774,8 @@ int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink
 
 int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                 cudaStream_t stream) {
-    if (count < 0 || what < 0 || what > 5 || (count > 0 && (!a || !out0))) return TP_EINVAL;
-    if ((what == 0 || what == 2) && count > 0 && !out1) return TP_EINVAL;
+    if (count < 0 || what < 0 || what > 7 || (count > 0 && (!a || !out0))) return TP_EINVAL;
+    if ((what == 0 || what == 2 || what == 6) && count > 0 && !out1) return TP_EINVAL;
     if (what == 2 && count > 0 && !b) return TP_EINVAL;
     cudaError_t e = tp::launch_debug(what, a, b, out0, out1, count, stream);
     return e == cudaSuccess ? TP_OK : cuda_fail(e);

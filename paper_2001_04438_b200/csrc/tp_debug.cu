@@ -25,6 +25,14 @@ __global__ void debug_kernel(int what, const float* a, const float* b, float* o0
         case 3: o0[i] = exp_flush2(make_float2(a[i], a[i])).x; break;
         case 4: o0[i] = ex2_ftz(a[i]); break;
         case 5: reinterpret_cast<unsigned long long*>(o0)[i] = globaltimer_ns(); break;  // timeline marker
+        case 6: {  // the hot path's ExtExp: ext_exp2v<false> (no clamp), n recovered from v
+            float2 m, v;
+            ext_exp2v<false>(make_float2(a[i], a[i]), m, v);
+            o0[i] = m.x;
+            o1[i] = __fsub_rn(v.x, kMagic);
+            break;
+        }
+        case 7: o0[i] = pow2_bits(__float2int_rn(a[i])); break;  // the hot path's 2^(d - 127)
         default: break;
     }
 }

@@ -1,10 +1,29 @@
 // Internal (C++) interface between the C ABI (tp_api.cu) and the kernels (tp_kernels.cu).
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace tp {
+
+// Development overrides (environment variables) exist only in builds compiled with
+// -DTP_DEV_OVERRIDES (tools/ A/B experiments); a release build always takes the default.
+inline int dev_env_int(const char* name, int dflt) {
+#ifdef TP_DEV_OVERRIDES
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
+}
+
+// Per-device launch-configuration caches, filled on first use (benign to compute twice; the
+// slots are atomics so concurrent host threads never race on them).
+constexpr int kMaxDevices = 64;
+using DevCache = std::atomic<int>;
 
 // Workspace header: the persistent kernels' work queue and launch epoch.  Zero-filled once at
 // allocation; every launch leaves it reusable (the last CTA resets the queue).
@@ -16,13 +35,32 @@ struct WsHeader {
     // watchdog: bit 0 = a wait for a row flag timed out.  Its own 128-byte line: every role
     // polls it while waiting, and the work-queue atomics on `counter` must not queue behind them
     alignas(128) unsigned error;
+    unsigned pad_;
+    // host-mapped abort word of this device (written by every launch before any wait can time
+    // out): raise_abort stores 1 into it so that the next C-ABI call reports TP_EWATCHDOG
+    unsigned* abort_host;
 };
 
-// Mailbox of the one-sided pair exchange: uint32 flags[world] at 0, error word at byte 240, then
-// float2 pairs[world][rows] (rank-major, the layout kFinish's pairs_in reads).
-constexpr size_t kMailboxHeader = 256;
-constexpr size_t kMailboxErrorWord = 240;
+// The host-mapped abort word of device `dev` (tp_api.cu; allocated on first use).
+unsigned* abort_word_device(int dev);
+
+// Mailbox of the one-sided pair exchange, double-buffered by epoch parity (an exchange of epoch e
+// uses half e & 1): uint32 flags[2][64] (half h at byte h * kMailboxFlagStride), the error word
+// at byte kMailboxErrorWord, then float2 pairs[2][world][rows] from byte kMailboxHeader (half h
+// at kMailboxHeader + h * world * rows * 8; rank-major, the layout kFinish's pairs_in reads).
+// Two halves suffice: a rank pushes epoch e + 2 only after its finish of e + 1, which waited
+// for every rank's push of e + 1, which each rank issues after its own finish of e; so no push
+// ever overwrites a half a peer's finish has not read.
+constexpr size_t kMailboxFlagStride = 256;
+constexpr size_t kMailboxErrorWord = 512;
+constexpr size_t kMailboxHeader = 1024;
 constexpr int kMailboxMaxWorld = 56;
+__host__ __device__ inline size_t mailbox_pairs_offset(int world, int64_t rows, unsigned epoch) {
+    return kMailboxHeader + (size_t)(epoch & 1u) * sizeof(float) * 2 * (size_t)world * (size_t)rows;
+}
+__host__ __device__ inline size_t mailbox_flag_offset(unsigned epoch, int rank) {
+    return (size_t)(epoch & 1u) * kMailboxFlagStride + sizeof(unsigned) * (size_t)rank;
+}
 
 constexpr unsigned long long kWaitTimeoutNs = 4000000000ull;  // 4 s: only a bug can wait this long
 
@@ -85,6 +123,16 @@ cudaError_t launch_debug(int what, const float* a, const float* b, float* out0, 
 cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t s);
 cudaError_t launch_phase_only(int algo, int in_bf16, int phase, const void* x, float* y, int64_t rows, int64_t cols,
                               void* ws, const LaunchOpts& o, cudaStream_t s);
+// Sharded Three-Pass (softmax3_max_partial_ex / _sum_partial_ex / _finish_ex): one phase of the
+// comparator over the local chunk, statistics from the world's gathered partials.
+struct Shard3 {
+    const float* maxes = nullptr;  // world x rows (phases 1, 2)
+    const float* sums = nullptr;   // world x rows (phase 2)
+    int world = 1;
+    float* out = nullptr;          // rows: this chunk's max (phase 0) / sum (phase 1)
+};
+cudaError_t launch_shard3(int algo, int in_bf16, int phase, const void* x, float* y, int64_t rows, int64_t cols,
+                          void* ws, const Shard3& sh, const LaunchOpts& o, cudaStream_t s);
 cudaError_t launch_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, float* y,
                               cudaStream_t s);
 cudaError_t launch_exp_sweep(int what, uint32_t bits0, int64_t count, float* o0, float* o1, cudaStream_t s);

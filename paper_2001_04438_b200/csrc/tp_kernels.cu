@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kThreads, 1) general_kernel(const KArgs a) {
     __shared__ unsigned s_mask, s_epoch;
     __shared__ int64_t s_cur_row;
 
+    publish_abort_word(a);
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     const unsigned* row_ready = reinterpret_cast<const unsigned*>(a.ws + a.lay.row_ready);
     const In* x = static_cast<const In*>(a.x);
@@ -53,7 +54,18 @@ __global__ void __launch_bounds__(kThreads, 1) general_kernel(const KArgs a) {
     auto fetch = [&](int b) {
         const long long item = (long long)atomicAdd(&hdr->counter, 1ull);
         s_item[b] = item;
-        if (item < a.total_items) s_dec[b] = decode_item<A>(item, a.rows, a.nb, a.L);
+        if (item < a.total_items) {
+            if (a.phase_only) {  // one phase alone: items are (row, blk), odd phases backwards
+                Item it;
+                it.phase = a.phase_only - 1;
+                it.row = item / a.nb;
+                it.blk = item - it.row * a.nb;
+                if (it.phase & 1) it.blk = a.nb - 1 - it.blk;
+                s_dec[b] = it;
+            } else {
+                s_dec[b] = decode_item<A>(item, a.rows, a.nb, a.L);
+            }
+        }
     };
     if (threadIdx.x == 0) {
         if (A == kFinish && a.mailbox) finish_wait(a);  // fused NVLink exchange: the peers' pairs
@@ -81,9 +93,15 @@ __global__ void __launch_bounds__(kThreads, 1) general_kernel(const KArgs a) {
                         s_stats = finish_stats(a, it.row);
                         s_cur_row = it.row;
                     }
-                    s_mask = 0xffffffffu;  // the chunk's pass-1 clamp decisions are not known here
+                    s_mask = finish_mask(a, s_stats, it.row, it.blk);  // the partial's clamp decisions
+                } else if (a.shard_mu) {  // sharded Three-Pass phase: stats from the world's partials
+                    if (it.row != s_cur_row) {
+                        s_stats = shard_stats<A>(a, it.row, it.phase - 1);
+                        s_cur_row = it.row;
+                    }
+                    s_mask = 0u;
                 } else {
-                    wait_flag(row_ready + it.row * 2 + (it.phase - 1), want, &hdr->error);
+                    if (!a.phase_only) wait_flag(row_ready + it.row * 2 + (it.phase - 1), want, &hdr->error);
                     float4 st;
                     unsigned mask;
                     item_stats<A>(a, it, &st, &mask);
@@ -112,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) general_kernel(const KArgs a) {
                 op_pass2<V>(r, st, my_clamp, yb, valid, vec);
             }
         } else if constexpr (A == kFinish) {
-            op_pass2<V>(r, st, true, yb, valid, vec);
+            op_pass2<V>(r, st, my_clamp, yb, valid, vec);
         } else {
             if (it.phase == 0) {
                 op_max<V>(r, valid, s_part);
@@ -141,11 +159,15 @@ unsigned long long* profile_buffer() { return g_prof; }
 thread_local Plan g_plan;
 Plan& last_plan() { return g_plan; }
 
-static int g_num_sms[64];
+static DevCache g_num_sms[kMaxDevices];
 
 int device_sms(int dev) {
-    if (!g_num_sms[dev]) cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-    return g_num_sms[dev];
+    int n = g_num_sms[dev].load(std::memory_order_relaxed);
+    if (!n) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev].store(n, std::memory_order_relaxed);
+    }
+    return n;
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -170,13 +192,15 @@ static cudaError_t launch_general(KArgs a, const LaunchOpts& o, cudaStream_t s) 
     int dev = 0;
     cudaGetDevice(&dev);
     auto kern = general_kernel<In, A>;
-    static int occ[64];
-    if (!occ[dev]) {
+    static DevCache occ[kMaxDevices];
+    int occ_d = occ[dev].load(std::memory_order_relaxed);
+    if (!occ_d) {
         int n = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, 0);
-        occ[dev] = n > 0 ? n : 1;
+        occ_d = n > 0 ? n : 1;
+        occ[dev].store(occ_d, std::memory_order_relaxed);
     }
-    const int64_t resident = (int64_t)device_sms(dev) * occ[dev];
+    const int64_t resident = (int64_t)device_sms(dev) * occ_d;
     int64_t grid = o.grid_ctas > 0 ? o.grid_ctas : resident;
     if (grid > resident) grid = resident;
     if (grid > a.total_items) grid = a.total_items;
@@ -200,7 +224,7 @@ struct SideStream {
     cudaStream_t st = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
-static SideStream g_side[64];
+static SideStream g_side[kMaxDevices];
 
 template <typename In>
 static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_ctas, int side_cl,
@@ -270,12 +294,14 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
     a.pairs_in = pairs_in;
     a.world = world;
     a.vec = vec_ok<In>(x, y, cols);
-    static const int hints = [] {
-        const char* e = getenv("TP_L2_HINTS");
-        return e ? atoi(e) : 1;
-    }();
+    static const int hints = dev_env_int("TP_L2_HINTS", 1);
     a.l2_hints = hints;
     a.prof = profile_buffer();
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        a.abort_host = abort_word_device(dev);
+    }
     if (a.vec && !o.no_tma) {
         // a few rows of 1..3 blocks: one CTA per row, the row staged in shared memory
         // (the Three-Pass comparators too, so that they are compared on the same footing)
@@ -320,7 +346,7 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
 // in the workspace instead of waiting for them.
 template <typename In, int A>
 static cudaError_t launch_phase(const void* x, float* y, int64_t rows, int64_t cols, void* ws, int phase,
-                                const LaunchOpts& o, cudaStream_t s) {
+                                const LaunchOpts& o, cudaStream_t s, const Shard3* sh = nullptr) {
     KArgs a{};
     a.x = x; a.y = y; a.rows = rows; a.cols = cols;
     a.nb = (cols + kBlockElems - 1) / kBlockElems;
@@ -333,8 +359,32 @@ static cudaError_t launch_phase(const void* x, float* y, int64_t rows, int64_t c
     a.l2_hints = 1;
     a.prof = profile_buffer();
     a.phase_only = phase + 1;
-    if (!a.vec || phase < 0 || phase >= AlgoTraits<A>::P) return cudaErrorNotSupported;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        a.abort_host = abort_word_device(dev);
+    }
+    if (phase < 0 || phase >= AlgoTraits<A>::P) return cudaErrorNotSupported;
+    if (sh) {
+        a.world = sh->world;
+        a.shard_mu = sh->maxes;
+        a.shard_sigma = sh->sums;
+        a.shard_out = sh->out;
+        if (!a.vec || o.no_tma) return launch_general<In, A>(a, o, s);
+    }
+    if (!a.vec) return cudaErrorNotSupported;
     return launch_stream<In, A>(a, o, s);
+}
+
+cudaError_t launch_shard3(int algo, int in_bf16, int phase, const void* x, float* y, int64_t rows, int64_t cols,
+                          void* ws, const Shard3& sh, const LaunchOpts& o, cudaStream_t s) {
+    switch (algo * 2 + (in_bf16 ? 1 : 0)) {
+        case kRecompute * 2: return launch_phase<float, kRecompute>(x, y, rows, cols, ws, phase, o, s, &sh);
+        case kRecompute * 2 + 1: return launch_phase<uint16_t, kRecompute>(x, y, rows, cols, ws, phase, o, s, &sh);
+        case kReload * 2: return launch_phase<float, kReload>(x, y, rows, cols, ws, phase, o, s, &sh);
+        case kReload * 2 + 1: return launch_phase<uint16_t, kReload>(x, y, rows, cols, ws, phase, o, s, &sh);
+        default: return cudaErrorNotSupported;
+    }
 }
 
 cudaError_t launch_phase_only(int algo, int in_bf16, int phase, const void* x, float* y, int64_t rows, int64_t cols,

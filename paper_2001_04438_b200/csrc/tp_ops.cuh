@@ -93,10 +93,10 @@ __device__ __forceinline__ float2 block_value(const KArgs& a, const Item& it, co
         const Pair bp = block_tree_warps(part.v);
         unsigned mask = 0;
         for (int w = 0; w < kWarps; ++w) mask |= (unsigned)part.cb[w] << w;
-        if (mask) {
-            reinterpret_cast<unsigned*>(a.ws + a.lay.block_clamp)[it.row * a.nb + it.blk] = mask;
-            atomicOr(reinterpret_cast<unsigned*>(a.ws + a.lay.row_clamp) + it.row, 1u);
-        }
+        // every block's mask is stored (0 included), so a row with some clamped block never
+        // reads another block's stale mask from an earlier launch
+        reinterpret_cast<unsigned*>(a.ws + a.lay.block_clamp)[it.row * a.nb + it.blk] = mask;
+        if (mask) atomicOr(reinterpret_cast<unsigned*>(a.ws + a.lay.row_clamp) + it.row, 1u);
         return make_float2(bp.m, bp.n);
     }
     if (kind == kRedMax) {
@@ -116,14 +116,16 @@ __device__ __forceinline__ float2 block_value(const KArgs& a, const Item& it, co
 // stores, each fenced before its count, precede the flag).  The count returns to 0 for the next
 // launch.
 __device__ __forceinline__ void push_row_pair(const KArgs& a, int64_t row, float2 root) {
+    const size_t off = mailbox_pairs_offset(a.world, a.rows, a.xepoch);
     for (int p = 0; p < a.world; ++p)
-        reinterpret_cast<float2*>(a.peers[p] + kMailboxHeader)[(int64_t)a.rank * a.rows + row] = root;
+        reinterpret_cast<float2*>(a.peers[p] + off)[(int64_t)a.rank * a.rows + row] = root;
     __threadfence_system();
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     if (atomicAdd(&hdr->rows_done, 1u) == (unsigned)(a.rows - 1)) {
         hdr->rows_done = 0u;
         __threadfence_system();
-        for (int p = 0; p < a.world; ++p) st_release_sys(reinterpret_cast<unsigned*>(a.peers[p]) + a.rank, a.xepoch);
+        for (int p = 0; p < a.world; ++p)
+            st_release_sys(reinterpret_cast<unsigned*>(a.peers[p] + mailbox_flag_offset(a.xepoch, a.rank)), a.xepoch);
     }
 }
 
@@ -134,11 +136,11 @@ __device__ __forceinline__ void push_row_pair(const KArgs& a, int64_t row, float
 __device__ __forceinline__ void finish_wait(const KArgs& a) {
     const unsigned long long t0 = globaltimer_ns();
     for (int p = 0; p < a.world; ++p) {
-        const unsigned* flag = reinterpret_cast<const unsigned*>(a.mailbox) + p;
+        const unsigned* flag = reinterpret_cast<const unsigned*>(a.mailbox + mailbox_flag_offset(a.xepoch, p));
         while (ld_acquire_sys(flag) != a.xepoch) {
             if (globaltimer_ns() - t0 > a.wait_ns) {
                 atomicOr(reinterpret_cast<unsigned*>(const_cast<char*>(a.mailbox) + kMailboxErrorWord), 1u << (p & 31));
-                atomicOr(&reinterpret_cast<WsHeader*>(a.ws)->error, 1u);
+                raise_abort(&reinterpret_cast<WsHeader*>(a.ws)->error, 1u);
                 break;
             }
             __nanosleep(128);
@@ -199,9 +201,12 @@ __device__ void retire_batch(const KArgs& a, bool mine, const Item& it, float2 v
                 row_clamp[row] = 0u;
             }
             if (A == kPartial) {
+                // the chunk's clamp flag stays in the workspace for the finish launch on it
+                reinterpret_cast<float4*>(a.ws + a.lay.row_stats)[row * 2] = make_float4(root.x, root.y, clamped, 0.f);
                 if (a.pair_out) a.pair_out[row] = root;
                 if (a.peers) push_row_pair(a, row, root);
             } else {
+                if ((A == kRecompute || A == kReload) && a.shard_out) a.shard_out[row] = root.x;  // sharded
                 float4 st = row_stats_of<A>(phase, root, mu_l);
                 if (A == kTwoPass) st.z = clamped;
                 reinterpret_cast<float4*>(a.ws + a.lay.row_stats)[row * 2 + phase] = st;
@@ -233,14 +238,38 @@ __device__ __forceinline__ void item_stats(const KArgs& a, const Item& it, float
         *mask = __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) + it.row * a.nb + it.blk);
 }
 
-// kFinish: merge the world partials of a row with the canonical tree over rank index.
+// kFinish: merge the world partials of a row with the canonical tree over rank index.  .z: did
+// the partial launch on this workspace clamp any block of the row's chunk (reading G11; the
+// per-block masks are then in the workspace)?
 __device__ __forceinline__ float4 finish_stats(const KArgs& a, int64_t row) {
     const Pair root = seq_tree_pairs((int)next_pow2(a.world), [&](int i) {
         if (i >= a.world) return pair_identity();
         const float2 v = a.pairs_in[(int64_t)i * a.rows + row];
         return Pair{v.x, v.y};
     });
-    return make_float4(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m), 0.0f, 0.0f);
+    const float clamped = __ldcg(reinterpret_cast<const float4*>(a.ws + a.lay.row_stats) + row * 2).z;
+    return make_float4(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m), clamped, 0.0f);
+}
+
+// kFinish: the per-warp clamp decisions the partial launch took for this block (0 when no block
+// of the row's chunk was clamped).
+__device__ __forceinline__ unsigned finish_mask(const KArgs& a, const float4& st, int64_t row, int64_t blk) {
+    return st.z != 0.0f ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) + row * a.nb + blk) : 0u;
+}
+
+// Sharded Three-Pass: the statistics a phase needs from the world's gathered partials.  mu = the
+// max over ranks (exact); sigma = the canonical tree over rank index of the ranks' sums (reading
+// G8: with power-of-two worlds and chunks the ranks' sums are subtrees of the one-GPU tree, so
+// the result is bitwise that of one GPU).  dep_phase 0: (mu); 1: (mu, 1 / sigma, sigma).
+template <int A>
+__device__ __forceinline__ float4 shard_stats(const KArgs& a, int64_t row, int dep_phase) {
+    float mu = -__int_as_float(0x7f800000);
+    for (int w = 0; w < a.world; ++w) mu = fmaxf(mu, a.shard_mu[(int64_t)w * a.rows + row]);
+    if (dep_phase == 0) return make_float4(mu, 0.0f, 0.0f, 0.0f);
+    const float sigma = seq_tree_sum((int)next_pow2(a.world), [&](int i) {
+        return i < a.world ? a.shard_sigma[(int64_t)i * a.rows + row] : 0.0f;
+    });
+    return row_stats_of<A>(1, make_float2(sigma, 0.0f), mu);
 }
 
 template <int A>

@@ -96,7 +96,7 @@ __device__ __forceinline__ bool wait_cluster_or_abort(uint64_t* bar, uint32_t pa
         if ((i & 63u) == 0) {
             if (*reinterpret_cast<volatile unsigned*>(err)) return false;
             if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
-                atomicOr(err, bit);
+                raise_abort(err, bit);
                 return false;
             }
         }
@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     __shared__ __align__(8) uint64_t st_bar[2];            // count 1: row_st written
     __shared__ int p2_row;                                 // row iteration producer B has reached
 
+    publish_abort_word(a);
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     unsigned* err = &hdr->error;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 if ((i & 63u) == 63u) {
                     if (aborted(err)) return -1;
                     if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
-                        atomicOr(err, 128u);
+                        raise_abort(err, 128u);
                         return -1;
                     }
                 }
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 const unsigned long long t0 = globaltimer_ns();
                 for (unsigned i = 0; *reinterpret_cast<volatile int*>(&p2_row) < k - LA; ++i) {
                     if ((i & 63u) == 63u && (aborted(err) || globaltimer_ns() - t0 > kWaitTimeoutNs)) {
-                        atomicOr(err, 2048u);
+                        raise_abort(err, 2048u);
                         ok = false;
                         break;
                     }
@@ -493,9 +494,9 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
 // ----------------------------------------------------------------------------- host side
 template <typename In>
 static int max_active_clusters(int dev, int CL, size_t dyn) {
-    static int cache[64][5];
+    static DevCache cache[kMaxDevices][5];
     const int ci = CL == 1 ? 0 : CL == 2 ? 1 : CL == 4 ? 2 : CL == 8 ? 3 : 4;
-    if (cache[dev][ci]) return cache[dev][ci] > 0 ? cache[dev][ci] : 0;
+    if (const int c = cache[dev][ci].load(std::memory_order_relaxed)) return c > 0 ? c : 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(CL * 8));
     cfg.blockDim = dim3(kClThreads);
@@ -512,7 +513,7 @@ static int max_active_clusters(int dev, int CL, size_t dyn) {
         cudaGetLastError();
         n = -1;
     }
-    cache[dev][ci] = n;
+    cache[dev][ci].store(n, std::memory_order_relaxed);
     return n > 0 ? n : 0;
 }
 
@@ -523,14 +524,14 @@ static size_t rowcl_dyn_smem() {
 
 template <typename In>
 static void rowcl_configure(int dev) {
-    static int configured[64];
-    if (!configured[dev]) {
+    static DevCache configured[kMaxDevices];
+    if (!configured[dev].load(std::memory_order_acquire)) {
         cudaFuncSetAttribute(rowcl_kernel<In, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
         cudaFuncSetAttribute(rowcl_kernel<In, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowcl_dyn_smem<In>());
         // clusters of 16 CTAs (non-portable; one per GPC on B200)
         cudaFuncSetAttribute(rowcl_kernel<In, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(rowcl_kernel<In, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        configured[dev] = 1;
+        configured[dev].store(1, std::memory_order_release);
     }
 }
 
@@ -586,10 +587,7 @@ int rowcl_choose(int64_t rows, int64_t nb, int force_cl, bool vs_stream, int64_t
         const int64_t idle = (int64_t)sms - (int64_t)Q * CL;
         int64_t split = 0;
         int split_cl = 0;
-        static const int env_split = [] {  // development: TP_CL_SPLIT=1 also splits forced sizes
-            const char* e = getenv("TP_CL_SPLIT");
-            return e ? atoi(e) : 0;
-        }();
+        static const int env_split = dev_env_int("TP_CL_SPLIT", 0);  // development: also split forced sizes
         if ((env_split || (!force_cl && vs_stream)) && full > 0 && idle >= 8) {
             int cls = 1;
             while ((nb + cls - 1) / cls > kClMaxLocal) cls *= 2;
@@ -659,19 +657,13 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    // development overrides: TP_CL_POOL_A = half-stages of the pass-1 pool, TP_CL_LEAD = rows
-    // producer A may run ahead of producer B
-    static const int env_sa = [] {
-        const char* e = getenv("TP_CL_POOL_A");
-        return e ? atoi(e) : -1;
-    }();
-    static const int env_la = [] {
-        const char* e = getenv("TP_CL_LEAD");
-        return e ? atoi(e) : -1;
-    }();
+    // Pools and lead are fixed: half the half-stages to each pool and producer A at most one row
+    // ahead of producer B.  kClMinLocal (the shortest share a CTA may get) is derived from exactly
+    // these values (the tree warp never laps team B's statistics barrier): no override.
     constexpr int S2 = ClRing<In>::S2;
-    const int SA = env_sa >= 2 && env_sa <= S2 - 2 ? env_sa : S2 / 2;
-    const int LA = env_la >= 1 ? env_la : 1;
+    constexpr int SA = S2 / 2;
+    constexpr int LA = 1;
+    static_assert(2 * kClMinLocal<In> > S2 - SA, "a share must exceed the pass-2 pool");
     last_plan() = Plan{3, kTwoPass, ncl * CL, CL, 0, SA};  // lookahead_rows: side rows (launch_split)
     if (a.prof) return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, true>, a, CL, SA, LA);
     return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, false>, a, CL, SA, LA);

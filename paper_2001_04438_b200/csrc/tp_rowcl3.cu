@@ -36,7 +36,7 @@ __device__ __forceinline__ bool cl3_wait(uint64_t* bar, uint32_t parity, unsigne
         if ((i & 63u) == 0) {
             if (aborted(err)) return false;
             if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
-                atomicOr(err, bit);
+                raise_abort(err, bit);
                 return false;
             }
         }
@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(kCl3Threads, 1) rowcl3_kernel(const KArgs a, i
     __shared__ float2 gvals[kCl3MaxNb / kGroupBlocks];
     __shared__ float4 s_st;
 
+    publish_abort_word(a);
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     unsigned* err = &hdr->error;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -197,9 +198,9 @@ static size_t rowcl3_dyn(int in_bytes) { return (size_t)(in_bytes == 4 ? 3 : 6) 
 
 template <typename In, int A>
 static int rowcl3_clusters(int dev, int CL) {
-    static int cache[64][5];
+    static DevCache cache[kMaxDevices][5];
     const int ci = CL == 1 ? 0 : CL == 2 ? 1 : CL == 4 ? 2 : CL == 8 ? 3 : 4;
-    if (cache[dev][ci]) return cache[dev][ci] > 0 ? cache[dev][ci] : 0;
+    if (const int c = cache[dev][ci].load(std::memory_order_relaxed)) return c > 0 ? c : 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(CL * 8));
     cfg.blockDim = dim3(kCl3Threads);
@@ -216,7 +217,7 @@ static int rowcl3_clusters(int dev, int CL) {
         cudaGetLastError();
         n = -1;
     }
-    cache[dev][ci] = n;
+    cache[dev][ci].store(n, std::memory_order_relaxed);
     return n > 0 ? n : 0;
 }
 
@@ -226,12 +227,12 @@ cudaError_t launch_rowcl3(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) 
         return cudaErrorNotSupported;
     int dev = 0;
     cudaGetDevice(&dev);
-    static int configured[64];
-    if (!configured[dev]) {
+    static DevCache configured[kMaxDevices];
+    if (!configured[dev].load(std::memory_order_acquire)) {
         cudaFuncSetAttribute(rowcl3_kernel<In, A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)rowcl3_dyn(sizeof(In)));
         cudaFuncSetAttribute(rowcl3_kernel<In, A>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        configured[dev] = 1;
+        configured[dev].store(1, std::memory_order_release);
     }
     int Q = rowcl3_clusters<In, A>(dev, CL);
     if (Q < 1) return cudaErrorNotSupported;

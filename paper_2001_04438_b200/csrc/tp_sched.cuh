@@ -68,7 +68,33 @@ struct KArgs {
     const char* mailbox;     // kFinish: the local mailbox whose flags are awaited in-kernel, or null
     unsigned long long wait_ns;  // kFinish: give up (error bits) after this long
     unsigned long long* prof;  // development: per-role cycle counters (tp_set_profile_buffer), or null
+    unsigned* abort_host;      // host-mapped abort word of the device (WsHeader::abort_host)
+    // sharded Three-Pass (softmax3_*_partial / finish, phase_only launches): the world's
+    // gathered per-row maxima and sums (world x rows, rank-major), and this launch's per-row
+    // result (max or sum of the local chunk), or null
+    const float* shard_mu;
+    const float* shard_sigma;
+    float* shard_out;
 };
+
+// Record a watchdog abort: the launch's error bit (every role polls it and leaves) and the
+// device's host-mapped word, so the next C-ABI call returns TP_EWATCHDOG (a plain system-scope
+// store of 1: idempotent, no host-memory atomics needed).  err is &WsHeader::error.
+__device__ __forceinline__ void raise_abort(unsigned* err, unsigned bit) {
+    atomicOr(err, bit);
+    const WsHeader* h = reinterpret_cast<const WsHeader*>(reinterpret_cast<const char*>(err) - offsetof(WsHeader, error));
+    unsigned* host = *reinterpret_cast<unsigned* const volatile*>(&h->abort_host);
+    if (host) {
+        *reinterpret_cast<volatile unsigned*>(host) = 1u;
+        __threadfence_system();
+    }
+}
+
+// First thread of a launch: publish the abort word in the workspace header it uses.
+__device__ __forceinline__ void publish_abort_word(const KArgs& a) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.ws)
+        reinterpret_cast<WsHeader*>(a.ws)->abort_host = a.abort_host;
+}
 
 // number of (phase, row) units in schedule slots < s.  Item arithmetic is 32-bit: a launch
 // has far fewer than 2^32 items (2^32 blocks would be 2^46 elements).
@@ -209,7 +235,7 @@ __device__ __forceinline__ bool wait_flag(const unsigned* f, unsigned want, unsi
         __nanosleep(ns);
         ns = ns < 1024 ? ns * 2 : ns;
         if (globaltimer_ns() - t0 > kWaitTimeoutNs) {  // never hang the GPU on a bug
-            atomicOr(err, 1u);
+            raise_abort(err, 1u);
             return false;
         }
     }
@@ -227,7 +253,7 @@ __device__ __forceinline__ bool wait_or_abort(uint64_t* bar, uint32_t parity, un
         if ((i & 63u) == 0) {
             if (*reinterpret_cast<volatile unsigned*>(err)) return false;
             if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
-                atomicOr(err, bit);
+                raise_abort(err, bit);
                 return false;
             }
         }

@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const KArgs a, int C
         for (int b = 0; b < kSmallMaxBlocks; ++b) mbar_init(&full_bar[b], 1);
         fence_mbar_init();
     }
-    __syncthreads();
+    // every CTA of the cluster has started (and initialised its barriers) before any CTA
+    // stores into a peer's shared memory (st.shared::cluster below)
+    cluster_sync_all();
     pdl_wait_and_release();  // programmatic launch: set up above, touch memory only after the predecessor
     unsigned iter = 0;
     for (int64_t row = cluster_id_x(); row < a.rows; row += nclusters_x(), ++iter) {
@@ -118,7 +120,9 @@ __global__ void __launch_bounds__(kThreads, 1) small3_kernel(const KArgs a, int 
         for (int b = 0; b < kSmallMaxBlocks; ++b) mbar_init(&full_bar[b], 1);
         fence_mbar_init();
     }
-    __syncthreads();
+    // every CTA of the cluster has started (and initialised its barriers) before any CTA
+    // stores into a peer's shared memory (st.shared::cluster below)
+    cluster_sync_all();
     pdl_wait_and_release();
     unsigned iter = 0, xchg = 0;
     // block values (warp 0) -> every cluster CTA, cluster barrier, row value (warp 0) -> s_st
@@ -220,12 +224,12 @@ cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     const size_t dyn = (size_t)per * kBlockElems * sizeof(In);
     auto kern = A == kTwoPass ? small_kernel<In> : (A == kRecompute ? small3_kernel<In, kRecompute>
                                                                      : small3_kernel<In, kReload>);
-    static int configured[64];
-    if (!configured[dev]) {
+    static DevCache configured[kMaxDevices];
+    if (!configured[dev].load(std::memory_order_acquire)) {
         for (auto k : {small_kernel<In>, small3_kernel<In, kRecompute>, small3_kernel<In, kReload>})
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(kSmallMaxBlocks * kBlockElems * sizeof(In)));
-        configured[dev] = 1;
+        configured[dev].store(1, std::memory_order_release);
     }
     int64_t nclu = o.grid_ctas > 0 ? o.grid_ctas / CL : sms / CL;
     if (nclu < 1) nclu = 1;
@@ -244,10 +248,7 @@ cudaError_t launch_small(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     // programmatic dependent launch: this grid may be scheduled while the previous kernel on
     // the stream runs (it waits for its completion before touching memory): the launch latency
     // of back-to-back short calls overlaps (development override TP_PDL=0)
-    static const int pdl = [] {
-        const char* e = getenv("TP_PDL");
-        return e ? atoi(e) : 1;
-    }();
+    static const int pdl = dev_env_int("TP_PDL", 1);
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;

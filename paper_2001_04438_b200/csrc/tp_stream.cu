@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
     __shared__ unsigned s_epoch;
 
     pdl_wait_and_release();  // programmatic launch: the previous grid on the stream is complete
+    publish_abort_word(a);
     WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     In* stages = reinterpret_cast<In*>(dsm);
@@ -191,13 +192,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
 
         // statistics of the row phase an item depends on, if released (cached per row)
         auto stats_ready = [&](const Item& it, int dep_phase, float4* st) -> bool {
-            if (!(it.row == cached_row && dep_phase == cached_phase)) {
+            if (!(it.row == cached_row && dep_phase == cached_phase) && a.shard_mu) {
+                cached_st = shard_stats<A>(a, it.row, dep_phase);  // sharded Three-Pass phase
+                cached_row = it.row;
+                cached_phase = dep_phase;
+            } else if (!(it.row == cached_row && dep_phase == cached_phase)) {
                 // phase_only: the statistics are those a previous full launch left in the workspace
                 if (!a.phase_only && ld_acquire_gpu(row_ready + it.row * 2 + dep_phase) != want) {
                     const unsigned long long now = globaltimer_ns();
                     if (wait_t0 == 0) wait_t0 = now;
                     if (now - wait_t0 <= kWaitTimeoutNs) return false;
-                    atomicOr(&hdr->error, 1u);  // never hang the GPU on a bug
+                    raise_abort(&hdr->error, 1u);  // never hang the GPU on a bug
                 }
                 if (a.prof && tl_rel == 0) tl_rel = globaltimer_ns();
                 cached_st = __ldcg(reinterpret_cast<const float4*>(a.ws + a.lay.row_stats) + it.row * 2 + dep_phase);
@@ -236,7 +241,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 it.phase = hold ? 0 : a.phase_only - 1;  // hold: pass 1 then pass 2 on the same stage
                 it.row = u / nb;
                 it.blk = u - (u / nb) * nb;
-                if (it.phase > 0) it.blk = a.nb - 1 - it.blk;
+                // hold: pass 2 backwards; one phase alone: odd phases backwards (each phase
+                // starts where the previous one ended, the L2-resident end)
+                if (hold ? it.phase > 0 : (it.phase & 1)) it.blk = a.nb - 1 - it.blk;
             } else if (item == dec_item + 1 && (uint64_t)item % (uint64_t)a.nb != 0) {
                 it = dec_it;  // the next block of the same (row, phase) unit (decode_item's direction)
                 it.blk += (A == kFinish || it.phase > 0) ? -1 : 1;
@@ -255,7 +262,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 mbar_arrive(&full_bar[s]);
             } else {
                 const uint32_t bytes = (uint32_t)valid * (uint32_t)sizeof(In);
-                const bool keep = !hold && !a.phase_only && ((P > 1 && it.phase < P - 1) || A == kPartial);
+                // evict_last for blocks a later pass re-reads: the interleaved schedule's early
+                // phases, the partial (the finish follows), a sharded Three-Pass phase but its last
+                const bool keep = !hold && (a.phase_only ? (a.shard_mu || a.shard_out) && it.phase < P - 1
+                                                         : ((P > 1 && it.phase < P - 1) || A == kPartial));
                 In* dst = stages + (size_t)s * kBlockElems;
                 const unsigned long long f0 = a.prof ? clock64() : 0ull;
                 fence_proxy_async_smem();
@@ -271,7 +281,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                     cached_row = it.row;
                 }
                 meta[s].stats = cached_st;
-                meta[s].mask = 0xffffffffu;  // the chunk's pass-1 clamp decisions are not known here
+                meta[s].mask = finish_mask(a, cached_st, it.row, it.blk);  // the partial's clamp decisions
             }
             if (hold) {
                 wait_stats(s);  // P1 now, P2 once the row is released
@@ -440,7 +450,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                 if (it.phase == 0) op_pass1<V>(v, valid, ps.part);  // kOpP1 (hold) or stream pass 1
                 else op_pass2<V>(v, st, my_clamp, yb, valid, true);
             } else if constexpr (A == kFinish) {
-                op_pass2<V>(v, st, true, yb, valid, true);
+                op_pass2<V>(v, st, my_clamp, yb, valid, true);
             } else {
                 if (it.phase == 0) op_max<V>(v, valid, ps.part);
                 else if (it.phase == 1) op_expsum<V, A == kReload>(v, valid, st.x, ps.part, yb, true);
@@ -473,10 +483,10 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     auto kern = stream_kernel<In, A>;
     constexpr int S = Ring<In>::S;
     const size_t dyn = (size_t)S * kBlockElems * sizeof(In);
-    static int configured[64];
-    if (!configured[dev]) {
+    static DevCache configured[kMaxDevices];
+    if (!configured[dev].load(std::memory_order_acquire)) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        configured[dev] = 1;
+        configured[dev].store(1, std::memory_order_release);
     }
     const int64_t resident = device_sms(dev);  // one CTA per SM
     int64_t grid = o.grid_ctas > 0 ? o.grid_ctas : resident;
@@ -492,10 +502,7 @@ cudaError_t launch_stream(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     last_plan() = Plan{2, A, grid, 0, a.L, a.hold};
     // programmatic dependent launch (the kernel waits for the previous grid before touching
     // memory): the launch overlaps the previous kernel's tail (development override TP_PDL=0)
-    static const int pdl = [] {
-        const char* e = getenv("TP_PDL");
-        return e ? atoi(e) : 1;
-    }();
+    static const int pdl = dev_env_int("TP_PDL", 1);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kStreamThreads);

@@ -102,3 +102,64 @@ def test_ipc_handles_gathered_rank_ordered():
         p.join(timeout=60)
     for r in range(2):
         assert res[r] == [bytes([0]) * 64, bytes([1]) * 64]
+
+
+# ---- the sharded Three-Pass orchestration (dist.chunk_sharded_softmax3) with gloo: the kernels
+# are replaced by plain CPU stand-ins of the same per-chunk contract (the host logic under test is
+# the sequence max partial -> gather -> sum partial -> gather -> finish and the rank order)
+
+def _fake_tp():
+    import types
+    import paper_2001_04438_b200 as real
+    f = types.SimpleNamespace(ALGO_RECOMPUTE=real.ALGO_RECOMPUTE, ALGO_RELOAD=real.ALGO_RELOAD)
+    f.softmax3_max_partial = lambda x, workspace=None: x.double().amax(dim=1).float()
+
+    def sum_partial(x, algo, maxes, out=None, workspace=None):
+        mu = maxes.amax(dim=0).double()
+        e = torch.exp(x.double() - mu[:, None])
+        if algo == real.ALGO_RELOAD:
+            out.copy_(e.float())
+        return e.sum(dim=1).float()
+
+    def finish(x, algo, maxes, sums, out=None, workspace=None):
+        mu = maxes.amax(dim=0).double()
+        sigma = sums.double().sum(dim=0)
+        e = torch.exp(x.double() - mu[:, None]) if algo == real.ALGO_RECOMPUTE else out.double()
+        out.copy_((e / sigma[:, None]).float())
+        return out
+    f.softmax3_sum_partial, f.softmax3_finish = sum_partial, finish
+    return f
+
+
+def _sharded3_worker(rank, world, port, q):
+    import sys
+    import paper_2001_04438_b200 as real
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        sys.modules["paper_2001_04438_b200"] = _fake_tp()
+        torch.manual_seed(0)
+        x = torch.randn(3, 40, dtype=torch.float64).float() * 30
+        c0, c1 = rank * 20, rank * 20 + 20
+        outs = {}
+        for algo in (real.ALGO_RECOMPUTE, real.ALGO_RELOAD):
+            outs[algo] = tpd.chunk_sharded_softmax3(x[:, c0:c1].contiguous(), algo).tolist()
+        want = torch.softmax(x.double(), dim=1)[:, c0:c1]
+        q.put((rank, [float((torch.tensor(v, dtype=torch.float64) - want).abs().max()) for v in outs.values()]))
+    finally:
+        sys.modules["paper_2001_04438_b200"] = real
+        dist.destroy_process_group()
+
+
+def test_chunk_sharded_three_pass_orchestration_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_sharded3_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        assert max(res[r]) < 1e-6, res[r]

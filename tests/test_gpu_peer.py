@@ -128,9 +128,11 @@ def test_fused_push_and_in_kernel_wait(world, rows, cols, dtype):
     boxes = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
     ex = [tpd.PeerPairExchange(rows, "cuda", rank=r, world=world, mailboxes=boxes) for r in range(world)]
     chunks = [c.contiguous() for c in _chunks(xd, world)]
+    wss = [tp.new_workspace(rows, max(c.shape[1], 1)) for c in chunks]  # one per emulated rank
     for _ in range(3):  # epochs 1, 2, 3 on the same mailboxes
-        epochs = [ex[r].push_partial(chunks[r]) for r in range(world)]
-        outs = [to_host(ex[r].finish(chunks[r], epochs[r])) for r in range(world) if chunks[r].shape[1]]
+        epochs = [ex[r].push_partial(chunks[r], wss[r]) for r in range(world)]
+        outs = [to_host(ex[r].finish(chunks[r], epochs[r], workspace=wss[r])) for r in range(world)
+                if chunks[r].shape[1]]
         assert tp.watchdog_flags() == 0 and all(e.error() == 0 for e in ex)
         # the mailbox holds exactly the pairs the unfused partial computes
         parts = torch.stack([tp.partial(c) if c.shape[1] else
@@ -156,3 +158,62 @@ def test_fused_finish_times_out_instead_of_hanging():
     assert tp.watchdog_flags() & 1    # reported (and cleared) by the watchdog
     y = tp.softmax(xd)                # the workspace is usable again afterwards
     assert_parity(to_host(xd), to_host(y), "after timeout")
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_mailbox_reuse_with_a_rank_one_epoch_ahead(fused):
+    # Rank A finishes epoch 1 and pushes epoch 2 (new data) before rank B's finish of epoch 1 has
+    # read the pairs: the epoch-parity halves keep B's epoch-1 pairs intact (a single-buffered
+    # mailbox fails here: B's flag wait sees epoch 2, or B reads A's epoch-2 pair).  Emulated
+    # ranks, one stream, every wait after the pushes it needs (no kernel waits on another).
+    world, rows, cols = 2, 3, 16384 * 8
+    xs = [workloads.ragged_case(rows, cols, -300, 300, seed=31 + e, stream=9) for e in (1, 2)]
+    xds = [to_dev(x) for x in xs]
+    refs = [to_host(tp.softmax(xd)) for xd in xds]
+    ch = [[c.contiguous() for c in _chunks(xd, world)] for xd in xds]
+    nbytes = tp.lib().tp_mailbox_bytes(world, rows)
+    boxes = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    ex = [tpd.PeerPairExchange(rows, "cuda", rank=r, world=world, mailboxes=boxes) for r in range(world)]
+    wss = [tp.new_workspace(rows, cols // world) for _ in range(world)]
+    if fused:
+        e1 = [ex[r].push_partial(ch[0][r], wss[r]) for r in range(world)]
+        ya1 = ex[0].finish(ch[0][0], e1[0], workspace=wss[0])
+        e2a = ex[0].push_partial(ch[1][0], wss[0])              # A one epoch ahead
+        yb1 = ex[1].finish(ch[0][1], e1[1], workspace=wss[1])  # B still on epoch 1
+        e2b = ex[1].push_partial(ch[1][1], wss[1])
+        ya2 = ex[0].finish(ch[1][0], e2a, workspace=wss[0])
+        yb2 = ex[1].finish(ch[1][1], e2b, workspace=wss[1])
+    else:
+        def part(e, r):
+            return tp.partial(ch[e][r], workspace=wss[r])
+        p1 = [part(0, r) for r in range(world)]
+        for r in range(world):
+            ex[r].push(p1[r], 1)
+        ya1 = tp.finish(ch[0][0], ex[0].wait(1), world, workspace=wss[0]).clone()
+        ex[0].push(part(1, 0), 2)                               # A one epoch ahead
+        yb1 = tp.finish(ch[0][1], ex[1].wait(1), world, workspace=wss[1]).clone()
+        ex[1].push(part(1, 1), 2)
+        ya2 = tp.finish(ch[1][0], ex[0].wait(2), world, workspace=wss[0])
+        yb2 = tp.finish(ch[1][1], ex[1].wait(2), world, workspace=wss[1])
+    torch.cuda.synchronize()
+    assert all(e.error() == 0 for e in ex) and tp.watchdog_flags() == 0
+    assert np.array_equal(np.concatenate([to_host(ya1), to_host(yb1)], axis=1), refs[0])
+    assert np.array_equal(np.concatenate([to_host(ya2), to_host(yb2)], axis=1), refs[1])
+
+
+def test_watchdog_abort_is_reported_by_the_next_call():
+    # a launch that gives up a wait (here: the fused finish whose peer never pushes) makes the
+    # NEXT call on the device fail with TP_EWATCHDOG; the call after that runs normally
+    rows, world = 2, 2
+    boxes = [torch.zeros(tp.lib().tp_mailbox_bytes(world, rows), dtype=torch.uint8, device="cuda")
+             for _ in range(world)]
+    ex = tpd.PeerPairExchange(rows, "cuda", rank=0, world=world, mailboxes=boxes, timeout_s=0.002)
+    x = workloads.ragged_case(rows, 16384 * 2, seed=24)
+    xd = to_dev(x)
+    ex.finish(xd, ex.push_partial(xd))  # rank 1 never pushes: the in-kernel wait gives up
+    torch.cuda.synchronize()
+    with pytest.raises(tp.TwoPassError, match="watchdog"):
+        tp.softmax(xd)
+    y = tp.softmax(xd)                  # state was reset by the reporting call
+    assert_parity(x, to_host(y), "after a reported abort")
+    assert tp.watchdog_flags() == 0

@@ -181,3 +181,33 @@ def test_exp_within_2_ulp_on_strided_fp32_sweep(what):
         err = np.abs(got.astype(np.longdouble) - ref).astype(np.float64) / _ulp32(ref.astype(np.float64))
         worst = max(worst, float(err.max()))
     assert worst < 2.0, worst
+
+
+# ------------------------------------------------------------------ the hot path's own forms (tp_debug_op 6, 7)
+
+def test_hot_path_extexp_matches_definition_and_the_scalar_form():
+    # op 6 = ext_exp2v<false>, exactly what pass 1 / pass 2 evaluate (FFMA2, n recovered from the
+    # rounding sum): (m, n) represents e^x, and inside the accuracy domain it
+    # is bit-identical to the clamped scalar ExtExp (op 0) the other unit tests grade
+    lim = float(2 ** 21)
+    x = np.concatenate([_sweep(), workloads.uniform(100000, -lim, lim, seed=12, stream=1)]).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    m6, n6 = (t.cpu().numpy() for t in tp.debug_op(6, xd))
+    m0, n0 = (t.cpu().numpy() for t in tp.debug_op(0, xd))
+    assert np.array_equal(m6.view(np.uint32), m0.view(np.uint32)) and np.array_equal(n6, n0)
+    want = oracle.exp_scaled(x, n6.astype(np.float64))
+    rel = np.abs((m6.astype(np.longdouble) - want) / want).astype(np.float64)
+    small = np.abs(x) <= 1e4
+    assert rel[small].max() <= 3.0e-7 and rel.max() <= 1e-5, (rel[small].max(), rel.max())
+    # n: nearest integer of the exact product x * RN32(log2 e) (reading G1)
+    n_exact = np.rint(x.astype(np.float64) * np.float64(np.float32(1.4426950408889634)))
+    assert np.all(np.abs(n6 - n_exact) <= 0.0)
+
+
+def test_hot_path_pow2_bits_exhaustive():
+    # op 7 = pow2_bits(d): 2^(d - 127) built in the exponent field (Alg. 3's rescaling factors,
+    # PAPER.md:161, 168), +0 for d <= 0 (flush below 2^-126); every d
+    d = np.arange(-2000, 255, dtype=np.float32)
+    got = tp.debug_op(7, torch.from_numpy(d).cuda())[0].cpu().numpy()
+    want = np.array([np.float32(2.0 ** (int(k) - 127)) if k >= 1 else np.float32(0.0) for k in d], np.float32)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

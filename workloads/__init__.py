@@ -131,6 +131,11 @@ def c5_tie_value(seed: int = 0) -> float:
     return _c5_tie_cache[seed]
 
 
+def set_c5_tie_value(v: float, seed: int = 0) -> None:
+    """Seed the cache with M computed elsewhere (multi-rank runs: rank 0 scans, broadcasts)."""
+    _c5_tie_cache[seed] = float(v)
+
+
 def generate(key: str, row0: int = 0, nrows: int | None = None, col0: int = 0,
              ncols: int | None = None, seed: int = 0, out: np.ndarray | None = None) -> np.ndarray:
     """Generate rows [row0, row0+nrows) x cols [col0, col0+ncols) of config `key`.
