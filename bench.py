@@ -226,7 +226,8 @@ def cpu_baseline(args, spec):
 # ---------------------------------------------------------------- our arm
 
 KERNEL_NAMES = {"stream": "tp::stream_kernel<{In},kTwoPass>", "cluster": "tp::rowcl_kernel<{In}>",
-                "general": "tp::general_kernel<{In},kTwoPass>", "small": "tp::small_kernel<{In}>"}
+                "general": "tp::general_kernel<{In},kTwoPass>", "small": "tp::small_kernel<{In}>",
+                "phase": "tp::rowph_kernel<{In},kTwoPass>"}
 
 
 def traffic_from_profiles(workload: str, kernel: str):

@@ -181,6 +181,9 @@ int tp_ipc_close(void* dev_ptr);
 #define TP_SCHED_CLUSTER 3
 #define TP_SCHED_SMALL 4  /* rows of 1..3 blocks: one CTA per row, the row staged in shared
                              memory (AUTO picks it for at most 2 x SMs such rows) */
+#define TP_SCHED_PHASE 5  /* a few very long rows (Two-Pass: at most 8 rows; partial / finish:
+                             any): one CTA per SM, a static schedule of all pass-1 blocks then
+                             all pass-2 blocks (AUTO picks it when every SM gets >= 16 blocks) */
 typedef struct {
     int64_t grid_ctas;
     int64_t lookahead_rows;
@@ -245,7 +248,8 @@ int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t c
 /* ---- status ---------------------------------------------------------------- */
 /* What the last launch issued by this host thread ran (diagnostics; no device work):
  * kernel = 1 general (any alignment), 2 stream (persistent grid), 3 cluster (one
- * thread-block cluster per row), 4 small (one CTA per row of <= 3 blocks); variant = the kernel's operation (0 Two-Pass, 1 partial,
+ * thread-block cluster per row), 4 small (one CTA per row of <= 3 blocks), 5 phase (static
+ * schedule of a few long rows; hold = its stages); variant = the kernel's operation (0 Two-Pass, 1 partial,
  * 2 Recompute, 3 Reload, 4 single-block rows, 5 finish); grid_ctas; cluster_size (kernel 3);
  * lookahead_rows (kernel 1/2; kernel 3: rows handed to a concurrent side launch on the SMs
  * the clusters leave idle, 0 if none); hold (kernel 2: blocks kept staged between the passes;

@@ -25,7 +25,7 @@ _SO = os.environ.get("TP_LIBRARY") or os.path.join(_PKG, "libtwopass.so")
 
 TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV, TP_EWATCHDOG = 0, 1, 2, 3, 4
 ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3
-SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER, SCHED_SMALL = 0, 1, 2, 3, 4  # twopass.h TP_SCHED_*
+SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER, SCHED_SMALL, SCHED_PHASE = 0, 1, 2, 3, 4, 5  # TP_SCHED_*
 IN_F32, IN_BF16 = 0, 1
 
 EXPORTS = [
@@ -55,7 +55,7 @@ class SoftmaxPlan(ctypes.Structure):
                 ("cluster_size", ctypes.c_int), ("lookahead_rows", ctypes.c_int64), ("hold", ctypes.c_int)]
 
 
-KERNEL_NAMES = {0: "none", 1: "general", 2: "stream", 3: "cluster", 4: "small"}
+KERNEL_NAMES = {0: "none", 1: "general", 2: "stream", 3: "cluster", 4: "small", 5: "phase"}
 
 _lib = None
 
@@ -207,7 +207,7 @@ def new_workspace(rows: int, cols: int, device=None) -> torch.Tensor:
 
 
 def partial(x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
-            grid_ctas: int = 0) -> torch.Tensor:
+            grid_ctas: int = 0, schedule: int = 0) -> torch.Tensor:
     """Pass 1 of Alg. 3 over a chunk of each row -> [rows, 2] fp32 (m_sum, n_sum)."""
     x = _prep(x)
     rows, cols = _rows_cols(x)
@@ -215,7 +215,7 @@ def partial(x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.T
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(),
                                                              workspace.numel() * workspace.element_size())
     st = lib().softmax_partial_ex(_in_dtype(x), x.data_ptr(), rows, cols, p.data_ptr(), ws_ptr, ws_bytes,
-                                  _opts(grid_ctas), _stream(x))
+                                  _opts(grid_ctas, schedule=schedule), _stream(x))
     _check(st, "partial")
     return p
 
@@ -225,7 +225,7 @@ def _ws(workspace: torch.Tensor | None):
 
 
 def finish(x: torch.Tensor, pairs: torch.Tensor, world: int, out: torch.Tensor | None = None,
-           grid_ctas: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
+           grid_ctas: int = 0, workspace: torch.Tensor | None = None, schedule: int = 0) -> torch.Tensor:
     """Merge `world` partials per row (pairs: [world, rows, 2]) and run pass 2 on the local chunk.
     `workspace`: the one the chunk's partial() used (None: the internal one, as partial's None)."""
     x = _prep(x)
@@ -234,7 +234,7 @@ def finish(x: torch.Tensor, pairs: torch.Tensor, world: int, out: torch.Tensor |
     assert pairs.numel() == world * rows * 2
     y = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
     st = lib().softmax_finish_ex(_in_dtype(x), x.data_ptr(), y.data_ptr(), rows, cols, pairs.data_ptr(), world,
-                                 *_ws(workspace), _opts(grid_ctas), _stream(x))
+                                 *_ws(workspace), _opts(grid_ctas, schedule=schedule), _stream(x))
     _check(st, "finish")
     return y
 

@@ -336,6 +336,17 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
                 cudaGetLastError();
             }
         }
+        // a few very long rows (and the chunks of sharded rows): the phase kernel's static
+        // schedule (tp_rowph.cu)
+        if constexpr (A == kTwoPass || A == kPartial || A == kFinish) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (o.schedule == 5 || (o.schedule == 0 && rowph_applies(A, a.rows, a.nb, device_sms(dev)))) {
+                const cudaError_t e = launch_rowph<In, A>(a, o, s);
+                if (e != cudaErrorNotSupported) return e;
+                cudaGetLastError();
+            }
+        }
         return launch_stream<In, A>(a, o, s);
     }
     return launch_general<In, A>(a, o, s);

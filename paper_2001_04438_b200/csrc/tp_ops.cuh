@@ -292,5 +292,8 @@ template <typename In>
 cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
 template <typename In, int A>
 cudaError_t launch_rowcl3(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
+bool rowph_applies(int A, int64_t rows, int64_t nb, int sms);
+template <typename In, int A>
+cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s);
 
 }  // namespace tp

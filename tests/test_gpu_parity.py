@@ -608,3 +608,46 @@ def test_randomised_soak_short():
     r = subprocess.run([sys.executable, "tools/soak.py", "--minutes", "0.33", "--seed", "11", "--clamp-frac", "0.3"],
                        cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# ------------------------------------------------------------------ phase kernel (static schedule, tp_rowph.cu)
+
+PHASE_SHAPES = [(1, 16384 * 300 + 5), (3, 16384 * 200), (1, 1 << 22), (2, 16384 * 149 + 4000), (8, 16384 * 40)]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", PHASE_SHAPES)
+def test_phase_schedule_bitwise_and_parity(rows, cols, dtype):
+    # the phase kernel (one CTA per SM, pass 1 of every block then pass 2, the block trees in a
+    # tree warp) computes what every other schedule computes, bit for bit (reading G8)
+    x = workloads.ragged_case(rows, cols, -2000.0, 2000.0, seed=rows + 7, stream=cols % 1000)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    y_stream = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    for grid in (0, 7, 148):
+        y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_PHASE, grid_ctas=grid))
+        assert tp.last_plan()["kernel"] == "phase"
+        assert np.array_equal(y, y_stream), grid
+    assert_parity(x, y_stream, f"phase {rows}x{cols} {dtype}")
+
+
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_phase_schedule_partial_finish(world):
+    # the chunk launches of a sharded row on the phase kernel: bitwise the one-GPU result (P9), the
+    # clamp decisions of out-of-domain blocks replayed from the partial's workspace
+    cols = 16384 * 512
+    x = workloads.ragged_case(1, cols, -1000.0, 1000.0, seed=71, stream=world)
+    x[0, 5 * 16384 + 100: 5 * 16384 + 200] = -3e6   # out of the accuracy domain: clamped warps
+    xd = to_dev(x)
+    ref = to_host(tp.softmax(xd))
+    from paper_2001_04438_b200 import dist as tpd
+    spans = [tpd.chunk_range(cols, world, r) for r in range(world)]
+    wss = [tp.new_workspace(1, b - a) for a, b in spans]
+    for sched in (tp.SCHED_PHASE, tp.SCHED_STREAM):
+        pairs = torch.stack([tp.partial(xd[:, a:b], workspace=w, schedule=sched)
+                             for (a, b), w in zip(spans, wss)]).contiguous()
+        y = torch.empty_like(xd)
+        for (a, b), w in zip(spans, wss):
+            tp.finish(xd[:, a:b], pairs, world, out=y[:, a:b], workspace=w, schedule=sched)
+        assert np.array_equal(to_host(y), ref), sched
