@@ -3,29 +3,33 @@
 // pass 2 of a row can start only after its whole pass 1 (lambda needs every
 // element) and each pass must run at the HBM rate on its own.
 //
-// One CTA per SM, a static schedule (no work queue): CTA c owns the items c, c + G, c + 2G, ...
-// of pass 1 (row-major (row, block)), then the same of pass 2 (each row's blocks backwards: the
-// end of pass 1 is what L2 still holds).  Everyone knows the order, so there are no commands:
+// One CTA per SM.  Items are the row-major (row, block) blocks of pass 1, then those of pass 2
+// (each row's blocks backwards: the end of pass 1 is what L2 still holds), handed out in order
+// by a work queue in chunks of kPhChunk items (the next chunk's atomic in flight).  A CTA runs
+// its items in the order it took them, every role walking the same stage ring:
 //
-//   producer (1 thread)   streams every item of the CTA, pass 1 then pass 2, through a ring of S
-//                         64 KB stages with one bulk (TMA) copy each, as soon as a stage frees;
-//                         pass-2 blocks are prefetched while the row's statistics are pending
-//   16 compute warps      pass 1: values to registers, stage released, the thread's (m, n) pair
-//                          written to a tree slot; pass 2:
+//   producer (1 thread)   takes items, writes each one's index beside its stage and starts one
+//                         bulk (TMA) copy per block as soon as the stage frees (pass-2 blocks are
+//                         prefetched while the row's statistics are pending); past the end, an
+//                         end mark
+//   16 compute warps      per stage, in order: pass 1: values to registers,
+//                         stage released, the warp's (m, n) pair (lanes, then the warp's lane
+//                         tree) written to a slot for the tree warp; pass 2:
 //                         once the row is released, y = (m lambda') 2^(n - n_sum + 1) stored
-//   tree warp             the block value from the slot's 512 thread pairs (the canonical tree of
-//                         every kernel: lanes of a warp, then warps; reading G8), then the grid
-//                         combine through tickets (tp_ops.cuh retire_batch): group of 64 blocks,
-//                         row; the row's statistics released with its epoch-tagged flag
+//   tree warp             the block value from the slot's 16 warp pairs (the canonical tree of
+//                         every kernel; reading G8), then the grid combine through tickets
+//                         (tp_ops.cuh retire_batch): group of 64 blocks, row; the row's
+//                         statistics released with its epoch-tagged flag
 //
-// The per-block work is exactly the other kernels' (thread_pass1, the same trees, op_pass2), so
-// outputs are bit-identical to them.  What changes is the cost per block: the compute warps do no
-// shuffle tree and wait on nothing but their stage, and the producer does one copy per block.
+// The per-block work is exactly the other kernels' (warp_pass1, the same trees, op_pass2), so
+// outputs are bit-identical to them.  What changes is the cost per block: no command ring or
+// per-item decisions (the order is the queue's), one copy per block for the producer, and the
+// retirement (fences, tickets) beside the compute warps.  A queue, not a static split: SMs do
+// not all stream at the same rate (a static split measured a few SMs 2x behind the median).
 //
-// Deadlock freedom: every CTA issues all its pass-1 items before any pass-2 item, and pass 1
-// waits on nothing outside the CTA, so every row's pass 1 completes once every CTA runs; the grid
-// is one CTA per SM with the shared memory of one CTA per SM, so all CTAs are resident together
-// (a launch that cannot be falls back to the stream kernel).  Every wait has the watchdog.
+// Deadlock freedom: items are taken in increasing order and a CTA runs its items in that order;
+// a pass-2 item is taken only after every pass-1 item has been taken, and pass 1 waits on nothing
+// outside its CTA, so every row's pass 1 completes.  Every wait has the watchdog.
 #include "tp_ops.cuh"
 
 namespace tp {
@@ -34,50 +38,34 @@ constexpr int kPhCompute = kWarps;         // 16 compute warps
 constexpr int kPhProducer = kWarps;        // warp 16
 constexpr int kPhTree = kWarps + 1;        // warp 17
 constexpr int kPhThreads = (kWarps + 2) * 32;
-constexpr int kPhSlots = 4;                // thread-pair slots between the compute warps and the tree warp
+constexpr int kPhSlots = 8;                // warp-pair slots between the compute warps and the tree warp
 constexpr int64_t kPhMaxRows = 8;          // Two-Pass: rows of one launch (pass 2 waits for whole rows)
+constexpr unsigned long long kPhChunk = 2; // items per queue claim
 
 template <typename In> struct PhRing { static constexpr int S = sizeof(In) == 4 ? 3 : 6; };  // 192 KB
 
-// Item k of this CTA in phase `phase`: (row, blk) of the phase's row-major item list.
-__device__ __forceinline__ Item ph_item(const KArgs& a, int phase, int64_t k) {
-    const int64_t g = (int64_t)blockIdx.x + k * (int64_t)gridDim.x;
+// Item `item` of the launch: pass-1 items [0, rows nb) row-major, then pass-2 items (blocks of a
+// row backwards).  A partial launch has only the first kind, a finish launch only the second.
+template <int A>
+__device__ __forceinline__ Item ph_decode(const KArgs& a, int64_t item) {
+    const int64_t n = a.rows * a.nb;
     Item it;
-    it.phase = phase;
+    it.phase = A == kFinish ? 1 : (item >= n ? 1 : 0);
+    const int64_t g = (A == kTwoPass && item >= n) ? item - n : item;
     it.row = g / a.nb;
     const int64_t b = g - it.row * a.nb;
-    it.blk = phase == 0 ? b : a.nb - 1 - b;
+    it.blk = it.phase == 0 ? b : a.nb - 1 - b;
     return it;
 }
 
-// Items of this CTA in one phase (rows * nb items over the grid).
-__device__ __forceinline__ int64_t ph_count(const KArgs& a) {
-    const int64_t n = a.rows * a.nb;
-    return n > (int64_t)blockIdx.x ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-}
-
-// The block value (one whole warp) from its 512 thread pairs, bit-identical to warp_tree_pairs
-// over each warp's 32 lanes followed by block_tree_warps over the 16 warps: lane l builds the
-// perfect tree over threads 16 l .. 16 l + 15 (warp l/2, half l%2: levels 1-4 of warp_tree_pairs),
-// then level 5 pairs the halves, then the warp roots (even lanes) form block_tree_warps' tree.
-// Result in lane 0.
-__device__ __forceinline__ Pair ph_block_tree(const Pair* tp) {
+// The block value (one whole warp) from its 16 warp pairs, bit-identical to block_tree_warps
+// (perfect tree over the warps in order; reading G8): lane w < 16 holds warp w's pair, lanes
+// 2o apart merge at level o.  Result in lane 0.
+__device__ __forceinline__ Pair ph_block_tree(const Pair* wp) {
     const int lane = threadIdx.x & 31;
-    const float4* p = reinterpret_cast<const float4*>(tp + 16 * lane);
-    Pair l[16];
+    Pair v = lane < kWarps ? wp[lane] : pair_identity();
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const float4 q = p[i];
-        l[2 * i] = Pair{q.x, q.y};
-        l[2 * i + 1] = Pair{q.z, q.w};
-    }
-#pragma unroll
-    for (int o = 1; o < 16; o <<= 1)
-#pragma unroll
-        for (int i = 0; i + o < 16; i += 2 * o) l[i] = pair_merge(l[i], l[i + o]);
-    Pair v = l[0];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {  // o = 1: the warp's halves; 2..16: warps 1, 2, 4, 8 apart
+    for (int o = 1; o < kWarps; o <<= 1) {
         Pair r;
         r.m = __shfl_down_sync(0xffffffffu, v.m, o);
         r.n = __shfl_down_sync(0xffffffffu, v.n, o);
@@ -86,16 +74,23 @@ __device__ __forceinline__ Pair ph_block_tree(const Pair* tp) {
     return v;
 }
 
+// Development (KArgs::prof, tools/prof_phase.py): per-role clock cycles summed over CTAs.
+enum PhProf : int {
+    kPhP1Full = 0, kPhP1Slot, kPhP1Work, kPhP2Stats, kPhP2Full, kPhP2Work,  // compute warp 0
+    kPhTreeWait, kPhTreeWork, kPhTreeRetire, kPhTreeBatches, kPhTreeBlocks,  // tree warp
+    kPhProdWait, kPhProdTotal, kPhComputeTotal, kPhTreeTotal, kPhCtas
+};
+
 template <typename In, int A>
 __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     constexpr int V = InTraits<In>::V;
     constexpr int S = PhRing<In>::S;
     constexpr int T = kPhSlots;
-    constexpr bool kPass1 = A == kTwoPass || A == kPartial;
-    constexpr bool kPass2 = A == kTwoPass || A == kFinish;
     extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ __align__(16) Pair tpairs[T][kThreads];
+    __shared__ __align__(16) Pair wpairs[T][kWarps];
     __shared__ unsigned char cbits[T][kWarps];
+    __shared__ long long slot_item[T];  // pass-1 item of a slot, -1 = end
+    __shared__ long long meta[S];       // item of a stage use, -1 = end
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
     __shared__ __align__(8) uint64_t tfull[T];
@@ -108,9 +103,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     unsigned* err = &hdr->error;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     In* stages = reinterpret_cast<In*>(dsm);
-    const int64_t n_items = ph_count(a);
-    const int64_t n1 = kPass1 ? n_items : 0;           // pass-1 items of this CTA
-    const int64_t n_all = n1 + (kPass2 ? n_items : 0);  // stage uses: pass 1 then pass 2
+    const long long total = a.total_items;
 
     if (threadIdx.x == 0) {
         s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
@@ -126,6 +119,22 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     }
     __syncthreads();
     const unsigned want = s_epoch + 1u;
+    // development profile: this thread's cycle counters (warp 0 lane 0, tree lane 0, producer)
+    const bool prof = a.prof != nullptr && lane == 0 && (warp == 0 || warp == kPhTree || warp == kPhProducer);
+    unsigned long long pc[16] = {};
+    const unsigned long long p_start = prof ? clock64() : 0ull;
+    // timeline (development): globaltimer per CTA at prof[16 + 5 c + {start, pass-1 end, stats seen,
+    // tree end, end}]
+    unsigned long long* tl = a.prof ? a.prof + 16 + 5 * blockIdx.x : nullptr;
+    if (tl && threadIdx.x == 0) tl[0] = globaltimer_ns();
+    unsigned long long p_t = p_start;
+    auto lap = [&](int slot) {
+        if (prof) {
+            const unsigned long long now = clock64();
+            pc[slot] += now - p_t;
+            p_t = now;
+        }
+    };
 
     if (warp == kPhProducer) {
         // =============================================================== producer (lane 0)
@@ -134,120 +143,163 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
             // pass-1 blocks of a Two-Pass / partial launch are re-read (pass 2 / the finish
             // launch): keep them in L2; pass-2 reads are the last
             const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
-            for (int64_t k = 0; k < n_all; ++k) {
+            unsigned long long next = atomicAdd(&hdr->counter, kPhChunk);
+            unsigned long long end = next + kPhChunk;
+            unsigned long long ahead = atomicAdd(&hdr->counter, kPhChunk);  // used one chunk later
+            for (long long k = 0;; ++k) {
                 const int s = (int)(k % S);
+                lap(kPhProdTotal);
                 if (k >= S && !wait_or_abort(&empty_bar[s], (uint32_t)(((k / S) - 1) & 1), err, 64u)) break;
-                const bool p1 = k < n1;
-                const Item it = ph_item(a, p1 ? 0 : 1, p1 ? k : k - n1);
+                lap(kPhProdWait);
+                if (next == end) {
+                    next = ahead;
+                    end = next + kPhChunk;
+                    ahead = atomicAdd(&hdr->counter, kPhChunk);
+                }
+                const long long item = (long long)next++;
+                if (item >= total) {  // end mark for the compute warps
+                    meta[s] = -1;
+                    mbar_arrive(&full_bar[s]);
+                    break;
+                }
+                meta[s] = item;
+                const Item it = ph_decode<A>(a, item);
                 const int64_t e0 = it.blk * kBlockElems;
                 const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(&full_bar[s], bytes);
                 tma_load_1d(stages + (size_t)s * kBlockElems, x + it.row * a.cols + e0, bytes, &full_bar[s],
-                            p1 ? pol_keep : pol_drop);
+                            it.phase == 0 ? pol_keep : pol_drop);
             }
+            if (ahead == ~0ull) hdr->error |= 2u;  // consume the prefetched claim before leaving
         }
     } else if (warp == kPhTree) {
         // =============================================================== tree warp (pass 1)
-        for (int64_t k = 0; k < n1;) {
+        for (long long k = 0; A != kFinish;) {
             int n = 0;
             if (lane == 0) {
                 if (wait_or_abort(&tfull[k % T], (uint32_t)((k / T) & 1), err, 32u)) {
                     n = 1;
-                    while (n < T && k + n < n1 && mbar_test_parity(&tfull[(k + n) % T], (uint32_t)(((k + n) / T) & 1)))
-                        ++n;
+                    while (n < T && mbar_test_parity(&tfull[(k + n) % T], (uint32_t)(((k + n) / T) & 1))) ++n;
                 }
             }
             n = __shfl_sync(0xffffffffu, n, 0);
             if (n == 0) break;  // aborted
-            // the n blocks' values: lane j keeps block k + j's
+            lap(kPhTreeWait);
+            // the n slots' blocks (up to an end mark): lane j keeps block k + j's value
+            const long long my_item = lane < n ? slot_item[(k + lane) % T] : -1;
+            const unsigned stop = __ballot_sync(0xffffffffu, lane < n && my_item < 0);
+            const int m = stop ? __ffs(stop) - 1 : n;  // slots before the end mark
             float2 val = make_float2(0.f, 0.f);
             unsigned mask = 0;
-            for (int j = 0; j < n; ++j) {
+            for (int j = 0; j < m; ++j) {
                 const int t = (int)((k + j) % T);
-                const Pair bv = ph_block_tree(tpairs[t]);
+                const Pair bv = ph_block_tree(wpairs[t]);
                 const unsigned cb = lane < kWarps ? (unsigned)cbits[t][lane] : 0u;
-                const unsigned m = __ballot_sync(0xffffffffu, cb != 0) & ((1u << kWarps) - 1u);
+                const unsigned mm = __ballot_sync(0xffffffffu, cb != 0) & ((1u << kWarps) - 1u);
                 const float bm = __shfl_sync(0xffffffffu, bv.m, 0), bn = __shfl_sync(0xffffffffu, bv.n, 0);
                 if (lane == j) {
                     val = make_float2(bm, bn);
-                    mask = m;
+                    mask = mm;
                 }
             }
             __syncwarp();
-            if (lane < n) mbar_arrive(&tempty[(k + lane) % T]);  // the slots are free again
-            const bool mine = lane < n;
-            const Item it = ph_item(a, 0, k + (mine ? lane : 0));
+            if (lane < m) mbar_arrive(&tempty[(k + lane) % T]);  // the slots are free again
+            lap(kPhTreeWork);
+            const bool mine = lane < m;
+            const Item it = ph_decode<A>(a, mine ? my_item : 0);
             if (mine) {  // block_value's side effects: every block's clamp mask, the row's flag
                 reinterpret_cast<unsigned*>(a.ws + a.lay.block_clamp)[it.row * a.nb + it.blk] = mask;
                 if (mask) atomicOr(reinterpret_cast<unsigned*>(a.ws + a.lay.row_clamp) + it.row, 1u);
             }
             retire_batch<A == kFinish ? kTwoPass : A>(a, mine, it, val, 0.0f, want);
-            k += n;
+            lap(kPhTreeRetire);
+            pc[kPhTreeBatches] += 1;
+            pc[kPhTreeBlocks] += (unsigned long long)m;
+            k += m;
+            if (stop) break;
         }
     } else {
         // =============================================================== compute warps
-        int64_t k = 0;
-        bool ok = true;
-        for (; k < n1 && ok; ++k) {  // pass 1
+        const unsigned* row_ready = reinterpret_cast<const unsigned*>(a.ws + a.lay.row_ready);
+        long long ks = 0;  // tree slots used (pass-1 blocks)
+        int64_t cur_row = -1;
+        bool p1_done = false;
+        float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (long long k = 0;; ++k) {
             const int s = (int)(k % S);
-            const Item it = ph_item(a, 0, k);
+            lap(kPhP2Work);
+            if (!wait_or_abort(&full_bar[s], (uint32_t)((k / S) & 1), err, 4u)) break;
+            const long long item = meta[s];
+            if (item < 0) break;  // end mark
+            const Item it = ph_decode<A>(a, item);
             const int valid = (int)min((int64_t)kBlockElems, a.cols - it.blk * kBlockElems);
-            if (!wait_or_abort(&full_bar[s], (uint32_t)((k / S) & 1), err, 4u)) {
-                ok = false;
-                break;
-            }
             BlockVals v;
             load_stage<In>(stages + (size_t)s * kBlockElems, v);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[s]);  // the stage can be refilled
-            bool clamped;
-            const Pair tpr = thread_pass1<V>(v, valid, &clamped);
-            const int t = (int)(k % T);
-            if (k >= T && !wait_or_abort(&tempty[t], (uint32_t)(((k / T) - 1) & 1), err, 16u)) {
-                ok = false;
-                break;
-            }
-            tpairs[t][threadIdx.x] = tpr;
-            if (lane == 0) cbits[t][warp] = clamped ? 1 : 0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tfull[t]);
-        }
-        if (kPass2 && ok) {
-            const unsigned* row_ready = reinterpret_cast<const unsigned*>(a.ws + a.lay.row_ready);
-            int64_t cur_row = -1;
-            float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int64_t k2 = 0; k2 < n_items; ++k2, ++k) {  // pass 2
-                const int s = (int)(k % S);
-                const Item it = ph_item(a, 1, k2);
-                if (it.row != cur_row) {  // the row's statistics (released once its pass 1 is done)
-                    if (A == kFinish) {
-                        st = finish_stats(a, it.row);
-                    } else {
-                        if (lane == 0 && !wait_flag(row_ready + it.row * 2, want, err)) ok = false;
-                        ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
-                        if (!ok) break;
-                        st = __ldcg(reinterpret_cast<const float4*>(a.ws + a.lay.row_stats) + it.row * 2);
-                    }
-                    cur_row = it.row;
+            if (it.phase == 0) {  // pass 1
+                lap(kPhP1Full);
+                Pair wp;  // the warp's pair (thread pass 1, the warp's lane tree)
+                const bool clamped = warp_pass1<V>(v, valid, &wp);
+                const int t = (int)(ks % T);
+                lap(kPhP1Work);
+                if (ks >= T && !wait_or_abort(&tempty[t], (uint32_t)(((ks / T) - 1) & 1), err, 16u)) break;
+                lap(kPhP1Slot);
+                if (lane == 0) {
+                    wpairs[t][warp] = wp;
+                    cbits[t][warp] = clamped ? 1 : 0;
+                    if (warp == 0) slot_item[t] = item;
                 }
-                const unsigned mask = A == kFinish ? finish_mask(a, st, it.row, it.blk)
-                                                   : (st.z != 0.0f ? __ldcg(reinterpret_cast<const unsigned*>(
-                                                                             a.ws + a.lay.block_clamp) +
-                                                                         it.row * a.nb + it.blk)
-                                                                   : 0u);
-                const int valid = (int)min((int64_t)kBlockElems, a.cols - it.blk * kBlockElems);
-                if (!wait_or_abort(&full_bar[s], (uint32_t)((k / S) & 1), err, 4u)) break;
-                BlockVals v;
-                load_stage<In>(stages + (size_t)s * kBlockElems, v);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[s]);
-                op_pass2<V>(v, st, ((mask >> warp) & 1u) != 0, a.y + it.row * a.cols + it.blk * kBlockElems, valid,
-                            true);
+                if (lane == 0) mbar_arrive(&tfull[t]);
+                ++ks;
+                continue;
+            }
+            if (!p1_done && tl && threadIdx.x == 0) tl[1] = globaltimer_ns();
+            p1_done = true;
+            lap(kPhP2Full);
+            if (it.row != cur_row) {  // the row's statistics (released once its pass 1 is done)
+                if (A == kFinish) {
+                    st = finish_stats(a, it.row);
+                } else {
+                    bool ok = true;
+                    if (lane == 0) ok = wait_flag(row_ready + it.row * 2, want, err);
+                    if (!__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) break;
+                    st = __ldcg(reinterpret_cast<const float4*>(a.ws + a.lay.row_stats) + it.row * 2);
+                    if (tl && threadIdx.x == 0 && tl[2] == 0) tl[2] = globaltimer_ns();
+                }
+                cur_row = it.row;
+            }
+            const unsigned mask = A == kFinish ? finish_mask(a, st, it.row, it.blk)
+                                               : (st.z != 0.0f ? __ldcg(reinterpret_cast<const unsigned*>(
+                                                                         a.ws + a.lay.block_clamp) +
+                                                                     it.row * a.nb + it.blk)
+                                                               : 0u);
+            lap(kPhP2Stats);
+            op_pass2<V>(v, st, ((mask >> warp) & 1u) != 0, a.y + it.row * a.cols + it.blk * kBlockElems, valid, true);
+        }
+        // end mark for the tree warp (its loop stops at the first slot holding -1)
+        if (A != kFinish) {
+            const int t = (int)(ks % T);
+            if (!(ks >= T && !wait_or_abort(&tempty[t], (uint32_t)(((ks / T) - 1) & 1), err, 16u))) {
+                if (warp == 0 && lane == 0) slot_item[t] = -1;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tfull[t]);
             }
         }
     }
+    if (tl && warp == kPhTree && lane == 0) tl[3] = globaltimer_ns();
+    if (prof) {
+        lap(warp == 0 ? kPhP2Work : warp == kPhTree ? kPhTreeRetire : kPhProdTotal);
+        const int tot = warp == 0 ? kPhComputeTotal : warp == kPhTree ? kPhTreeTotal : kPhProdTotal;
+        pc[tot] = clock64() - p_start;
+        if (warp == 0) pc[kPhCtas] = 1;
+        for (int i = 0; i < 16; ++i)
+            if (pc[i]) atomicAdd(&a.prof[i], pc[i]);
+    }
     __syncthreads();
+    if (tl && threadIdx.x == 0) tl[4] = globaltimer_ns();
     if (threadIdx.x == 0) exit_and_reset(hdr);
 }
 
@@ -271,11 +323,11 @@ cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s) {
         configured[dev].store(1, std::memory_order_release);
     }
     if (resident[dev].load(std::memory_order_relaxed) < 1) return cudaErrorNotSupported;
-    // one CTA per SM, all resident (the static schedule's pass 2 waits for every CTA's pass 1)
+    // one CTA per SM
     int64_t grid = device_sms(dev);
     if (o.grid_ctas > 0 && o.grid_ctas < grid) grid = o.grid_ctas;
     if (grid > a.rows * a.nb) grid = a.rows * a.nb;
-    a.total_items = a.rows * a.nb;
+    a.total_items = a.rows * a.nb * (A == kTwoPass ? 2 : 1);
     last_plan() = Plan{5, A, grid, 0, 0, S};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);

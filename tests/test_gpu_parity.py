@@ -612,7 +612,7 @@ def test_randomised_soak_short():
 
 # ------------------------------------------------------------------ phase kernel (static schedule, tp_rowph.cu)
 
-PHASE_SHAPES = [(1, 16384 * 300 + 5), (3, 16384 * 200), (1, 1 << 22), (2, 16384 * 149 + 4000), (8, 16384 * 40)]
+PHASE_SHAPES = [(1, 16384 * 300 + 24), (3, 16384 * 200), (1, 1 << 22), (2, 16384 * 149 + 4000), (8, 16384 * 40)]
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -636,9 +636,14 @@ def test_phase_schedule_bitwise_and_parity(rows, cols, dtype):
 def test_phase_schedule_partial_finish(world):
     # the chunk launches of a sharded row on the phase kernel: bitwise the one-GPU result (P9), the
     # clamp decisions of out-of-domain blocks replayed from the partial's workspace
+    # row max near -2^21 with elements beyond the accuracy domain (reading G11): every 7th element
+    # at -3e6 inside in-domain warps (pass 1 unclamped: they weigh 0, and must stay 0), and whole
+    # blocks at -3e6 (their warps clamp to -2^21 in pass 1 and must clamp again in pass 2)
     cols = 16384 * 512
-    x = workloads.ragged_case(1, cols, -1000.0, 1000.0, seed=71, stream=world)
-    x[0, 5 * 16384 + 100: 5 * 16384 + 200] = -3e6   # out of the accuracy domain: clamped warps
+    x = workloads.ragged_case(1, cols, 0.0, 5.0, seed=71, stream=world) + np.float32(-2 ** 21 + 10)
+    x[0, ::7] = -3e6
+    x[0, 5 * 16384: 7 * 16384] = -3e6
+    x[0, 300 * 16384 + 8192: 301 * 16384] = -3e6
     xd = to_dev(x)
     ref = to_host(tp.softmax(xd))
     from paper_2001_04438_b200 import dist as tpd
