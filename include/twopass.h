@@ -182,8 +182,9 @@ int tp_ipc_close(void* dev_ptr);
 #define TP_SCHED_SMALL 4  /* rows of 1..3 blocks: one CTA per row, the row staged in shared
                              memory (AUTO picks it for at most 2 x SMs such rows) */
 #define TP_SCHED_PHASE 5  /* a few very long rows (Two-Pass: at most 8 rows; partial / finish:
-                             any): one CTA per SM, a static schedule of all pass-1 blocks then
-                             all pass-2 blocks (AUTO picks it when every SM gets >= 16 blocks) */
+                             any): one CTA per SM taking all pass-1 blocks, then all pass-2
+                             blocks, from an in-order queue, no command ring (AUTO picks it for
+                             the Two-Pass from ~100 blocks per SM, the partial from ~48) */
 typedef struct {
     int64_t grid_ctas;
     int64_t lookahead_rows;

@@ -40,7 +40,14 @@ constexpr int kPhTree = kWarps + 1;        // warp 17
 constexpr int kPhThreads = (kWarps + 2) * 32;
 constexpr int kPhSlots = 8;                // warp-pair slots between the compute warps and the tree warp
 constexpr int64_t kPhMaxRows = 8;          // Two-Pass: rows of one launch (pass 2 waits for whole rows)
-constexpr unsigned long long kPhChunk = 2; // items per queue claim
+#ifndef TP_PH_CHUNK
+#define TP_PH_CHUNK 2
+#endif
+#ifndef TP_PH_PREFETCH
+#define TP_PH_PREFETCH 0
+#endif
+constexpr unsigned long long kPhChunk = TP_PH_CHUNK;  // items per queue claim
+constexpr bool kPhPrefetch = TP_PH_PREFETCH != 0;     // L2 prefetch of the next claimed chunk
 
 template <typename In> struct PhRing { static constexpr int S = sizeof(In) == 4 ? 3 : 6; };  // 192 KB
 
@@ -48,13 +55,14 @@ template <typename In> struct PhRing { static constexpr int S = sizeof(In) == 4 
 // row backwards).  A partial launch has only the first kind, a finish launch only the second.
 template <int A>
 __device__ __forceinline__ Item ph_decode(const KArgs& a, int64_t item) {
-    const int64_t n = a.rows * a.nb;
+    // 32-bit arithmetic: a launch has far fewer than 2^31 blocks (2^31 blocks = 2^45 elements)
+    const uint32_t n = (uint32_t)(a.rows * a.nb), nb = (uint32_t)a.nb, i = (uint32_t)item;
     Item it;
-    it.phase = A == kFinish ? 1 : (item >= n ? 1 : 0);
-    const int64_t g = (A == kTwoPass && item >= n) ? item - n : item;
-    it.row = g / a.nb;
-    const int64_t b = g - it.row * a.nb;
-    it.blk = it.phase == 0 ? b : a.nb - 1 - b;
+    it.phase = A == kFinish ? 1 : (i >= n ? 1 : 0);
+    const uint32_t g = (A == kTwoPass && i >= n) ? i - n : i;
+    const uint32_t r = g / nb, b = g - r * nb;
+    it.row = r;
+    it.blk = it.phase == 0 ? b : nb - 1 - b;
     return it;
 }
 
@@ -91,6 +99,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     __shared__ unsigned char cbits[T][kWarps];
     __shared__ long long slot_item[T];  // pass-1 item of a slot, -1 = end
     __shared__ long long meta[S];       // item of a stage use, -1 = end
+    __shared__ Item meta_it[S];         // ... decoded (the producer decodes once per block)
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
     __shared__ __align__(8) uint64_t tfull[T];
@@ -155,6 +164,15 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                     next = ahead;
                     end = next + kPhChunk;
                     ahead = atomicAdd(&hdr->counter, kPhChunk);
+                    // the chunk after this one is known now: start its DRAM reads into L2, so that
+                    // more than the stage ring's bytes are in flight per SM (Little's law)
+                    if (kPhPrefetch)
+                        for (unsigned long long q = ahead; q < ahead + kPhChunk && q < (unsigned long long)total; ++q) {
+                            const Item pit = ph_decode<A>(a, (int64_t)q);
+                            const int64_t p0 = pit.blk * kBlockElems;
+                            bulk_prefetch_l2(x + pit.row * a.cols + p0,
+                                             (uint32_t)min((int64_t)kBlockElems, a.cols - p0) * (uint32_t)sizeof(In));
+                        }
                 }
                 const long long item = (long long)next++;
                 if (item >= total) {  // end mark for the compute warps
@@ -162,8 +180,9 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                     mbar_arrive(&full_bar[s]);
                     break;
                 }
-                meta[s] = item;
                 const Item it = ph_decode<A>(a, item);
+                meta[s] = item;
+                meta_it[s] = it;
                 const int64_t e0 = it.blk * kBlockElems;
                 const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
                 fence_proxy_async_smem();
@@ -232,7 +251,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
             if (!wait_or_abort(&full_bar[s], (uint32_t)((k / S) & 1), err, 4u)) break;
             const long long item = meta[s];
             if (item < 0) break;  // end mark
-            const Item it = ph_decode<A>(a, item);
+            const Item it = meta_it[s];
             const int valid = (int)min((int64_t)kBlockElems, a.cols - it.blk * kBlockElems);
             BlockVals v;
             load_stage<In>(stages + (size_t)s * kBlockElems, v);
@@ -342,12 +361,15 @@ cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-// Does the phase schedule apply (automatic choice)?  Rows long enough that every CTA gets many
-// blocks of each pass, few enough that a Two-Pass launch's pass 2 waiting for whole rows costs
-// nothing (the partial / finish launches have no such wait).
+// Does the phase schedule apply (automatic choice)?  Measured on B200 against the stream kernel
+// (tools/dev_sizes.py, one row of 2^26 .. 2^31 fp32 elements): the Two-Pass and the partial gain
+// from about 100 / 48 blocks per SM on (2^31: 4030 vs 4202 us, partial 1551 vs 1952 us); the
+// finish (pass 2 alone) is 0.4-1.6% faster on the stream kernel at every size, so AUTO keeps it
+// there.  A Two-Pass launch also needs few rows: its pass 2 waits for whole rows.
 bool rowph_applies(int A, int64_t rows, int64_t nb, int sms) {
-    if (A == kTwoPass && rows > kPhMaxRows) return false;
-    return rows * nb >= 16 * (int64_t)sms;
+    if (A == kTwoPass) return rows <= kPhMaxRows && rows * nb >= 100 * (int64_t)sms;
+    if (A == kPartial) return rows * nb >= 48 * (int64_t)sms;
+    return false;
 }
 
 #define TP_PH_INSTANTIATE(IN)                                                                  \
