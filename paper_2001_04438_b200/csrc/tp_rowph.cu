@@ -43,13 +43,18 @@ constexpr int64_t kPhMaxRows = 8;          // Two-Pass: rows of one launch (pass
 #ifndef TP_PH_CHUNK
 #define TP_PH_CHUNK 2
 #endif
-#ifndef TP_PH_PREFETCH
-#define TP_PH_PREFETCH 0
-#endif
 constexpr unsigned long long kPhChunk = TP_PH_CHUNK;  // items per queue claim
-constexpr bool kPhPrefetch = TP_PH_PREFETCH != 0;     // L2 prefetch of the next claimed chunk
 
-template <typename In> struct PhRing { static constexpr int S = sizeof(In) == 4 ? 3 : 6; };  // 192 KB
+// Staging: H half-block stages, H even, so that half-stage h always holds the same half of its
+// blocks (h even: first halves, read by warps 0-7; h odd: second halves, warps 8-15) and each
+// half frees as soon as its own 8 warps have read it: 6 x 32 KB fp32 / 12 x 16 KB bf16 = 192 KB.
+// (An odd H, 7 x 32 KB, would hold more bytes in flight, but then one half-stage serves both
+// halves in turn and the halves must stay in lockstep: measured 20% slower.)
+template <typename In> struct PhRing {
+    static constexpr int kHalf = kBlockElems / 2;
+    static constexpr int H = sizeof(In) == 4 ? 6 : 12;
+    static_assert(H % 2 == 0, "a half-stage must serve one half");
+};
 
 // Item `item` of the launch: pass-1 items [0, rows nb) row-major, then pass-2 items (blocks of a
 // row backwards).  A partial launch has only the first kind, a finish launch only the second.
@@ -92,16 +97,17 @@ enum PhProf : int {
 template <typename In, int A>
 __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     constexpr int V = InTraits<In>::V;
-    constexpr int S = PhRing<In>::S;
+    constexpr int H = PhRing<In>::H;          // half-stages
+    constexpr int HE = PhRing<In>::kHalf;     // elements per half-stage
     constexpr int T = kPhSlots;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ __align__(16) Pair wpairs[T][kWarps];
     __shared__ unsigned char cbits[T][kWarps];
     __shared__ long long slot_item[T];  // pass-1 item of a slot, -1 = end
-    __shared__ long long meta[S];       // item of a stage use, -1 = end
-    __shared__ Item meta_it[S];         // ... decoded (the producer decodes once per block)
-    __shared__ __align__(8) uint64_t full_bar[S];
-    __shared__ __align__(8) uint64_t empty_bar[S];
+    __shared__ long long meta[H];       // item of a half-stage use, -1 = end
+    __shared__ Item meta_it[H];         // ... decoded (the producer decodes once per block)
+    __shared__ __align__(8) uint64_t full_bar[H];
+    __shared__ __align__(8) uint64_t empty_bar[H];
     __shared__ __align__(8) uint64_t tfull[T];
     __shared__ __align__(8) uint64_t tempty[T];
     __shared__ unsigned s_epoch;
@@ -116,9 +122,9 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
 
     if (threadIdx.x == 0) {
         s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kPhCompute);
+        for (int h = 0; h < H; ++h) {
+            mbar_init(&full_bar[h], 1);
+            mbar_init(&empty_bar[h], kPhCompute / 2);  // the 8 warps of the half
         }
         for (int t = 0; t < T; ++t) {
             mbar_init(&tfull[t], kPhCompute);
@@ -155,40 +161,41 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
             unsigned long long next = atomicAdd(&hdr->counter, kPhChunk);
             unsigned long long end = next + kPhChunk;
             unsigned long long ahead = atomicAdd(&hdr->counter, kPhChunk);  // used one chunk later
-            for (long long k = 0;; ++k) {
-                const int s = (int)(k % S);
+            for (long long k = 0;; ++k) {  // block k: half-stages 2k, 2k + 1 of the ring
                 lap(kPhProdTotal);
-                if (k >= S && !wait_or_abort(&empty_bar[s], (uint32_t)(((k / S) - 1) & 1), err, 64u)) break;
+                const long long u0 = 2 * k;
+                const int h0 = (int)(u0 % H);
+                if (u0 >= H && !wait_or_abort(&empty_bar[h0], (uint32_t)(((u0 / H) - 1) & 1), err, 64u)) break;
                 lap(kPhProdWait);
                 if (next == end) {
                     next = ahead;
                     end = next + kPhChunk;
                     ahead = atomicAdd(&hdr->counter, kPhChunk);
-                    // the chunk after this one is known now: start its DRAM reads into L2, so that
-                    // more than the stage ring's bytes are in flight per SM (Little's law)
-                    if (kPhPrefetch)
-                        for (unsigned long long q = ahead; q < ahead + kPhChunk && q < (unsigned long long)total; ++q) {
-                            const Item pit = ph_decode<A>(a, (int64_t)q);
-                            const int64_t p0 = pit.blk * kBlockElems;
-                            bulk_prefetch_l2(x + pit.row * a.cols + p0,
-                                             (uint32_t)min((int64_t)kBlockElems, a.cols - p0) * (uint32_t)sizeof(In));
-                        }
                 }
                 const long long item = (long long)next++;
-                if (item >= total) {  // end mark for the compute warps
-                    meta[s] = -1;
-                    mbar_arrive(&full_bar[s]);
-                    break;
-                }
-                const Item it = ph_decode<A>(a, item);
-                meta[s] = item;
-                meta_it[s] = it;
+                const Item it = ph_decode<A>(a, item < total ? item : 0);
                 const int64_t e0 = it.blk * kBlockElems;
-                const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
-                fence_proxy_async_smem();
-                mbar_arrive_expect_tx(&full_bar[s], bytes);
-                tma_load_1d(stages + (size_t)s * kBlockElems, x + it.row * a.cols + e0, bytes, &full_bar[s],
-                            it.phase == 0 ? pol_keep : pol_drop);
+                const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
+                const In* src = x + it.row * a.cols + e0;
+                const uint64_t pol = it.phase == 0 ? pol_keep : pol_drop;
+                for (int j = 0; j < 2; ++j) {
+                    const long long u = u0 + j;
+                    const int h = (int)(u % H);
+                    if (j == 1 && u >= H && !wait_or_abort(&empty_bar[h], (uint32_t)(((u / H) - 1) & 1), err, 64u))
+                        break;
+                    const int n = item >= total ? 0 : min(HE, valid - j * HE);
+                    meta[h] = item >= total ? -1 : item;  // end mark in both halves
+                    meta_it[h] = it;
+                    if (n <= 0) {  // nothing to copy (end mark, or a short last block's 2nd half)
+                        mbar_arrive(&full_bar[h]);
+                        continue;
+                    }
+                    fence_proxy_async_smem();
+                    mbar_arrive_expect_tx(&full_bar[h], (uint32_t)n * (uint32_t)sizeof(In));
+                    tma_load_1d(stages + (size_t)h * HE, src + j * HE, (uint32_t)n * (uint32_t)sizeof(In),
+                                &full_bar[h], pol);
+                }
+                if (item >= total) break;
             }
             if (ahead == ~0ull) hdr->error |= 2u;  // consume the prefetched claim before leaving
         }
@@ -245,18 +252,21 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
         int64_t cur_row = -1;
         bool p1_done = false;
         float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int half = warp >= kWarps / 2 ? 1 : 0;  // the half of every block this warp reads
         for (long long k = 0;; ++k) {
-            const int s = (int)(k % S);
+            const long long u = 2 * k + half;
+            const int h = (int)(u % H);
             lap(kPhP2Work);
-            if (!wait_or_abort(&full_bar[s], (uint32_t)((k / S) & 1), err, 4u)) break;
-            const long long item = meta[s];
+            if (!wait_or_abort(&full_bar[h], (uint32_t)((u / H) & 1), err, 4u)) break;
+            const long long item = meta[h];
             if (item < 0) break;  // end mark
-            const Item it = meta_it[s];
+            const Item it = meta_it[h];
             const int valid = (int)min((int64_t)kBlockElems, a.cols - it.blk * kBlockElems);
             BlockVals v;
-            load_stage<In>(stages + (size_t)s * kBlockElems, v);
+            // the canonical layout addresses the whole block (second half at +HE): rebase
+            load_stage<In>(stages + (size_t)h * HE - (size_t)half * HE, v);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[s]);  // the stage can be refilled
+            if (lane == 0) mbar_arrive(&empty_bar[h]);  // the half-stage can be refilled
             if (it.phase == 0) {  // pass 1
                 lap(kPhP1Full);
                 Pair wp;  // the warp's pair (thread pass 1, the warp's lane tree)
@@ -327,8 +337,7 @@ cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     auto kern = rowph_kernel<In, A>;
-    constexpr int S = PhRing<In>::S;
-    const size_t dyn = (size_t)S * kBlockElems * sizeof(In);
+    const size_t dyn = (size_t)PhRing<In>::H * PhRing<In>::kHalf * sizeof(In);
     static DevCache configured[kMaxDevices];
     static DevCache resident[kMaxDevices];
     if (!configured[dev].load(std::memory_order_acquire)) {
@@ -347,7 +356,7 @@ cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     if (o.grid_ctas > 0 && o.grid_ctas < grid) grid = o.grid_ctas;
     if (grid > a.rows * a.nb) grid = a.rows * a.nb;
     a.total_items = a.rows * a.nb * (A == kTwoPass ? 2 : 1);
-    last_plan() = Plan{5, A, grid, 0, 0, S};
+    last_plan() = Plan{5, A, grid, 0, 0, PhRing<In>::H};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kPhThreads);
