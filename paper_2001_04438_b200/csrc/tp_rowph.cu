@@ -134,13 +134,18 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     }
     __syncthreads();
     const unsigned want = s_epoch + 1u;
-    // development profile: this thread's cycle counters (warp 0 lane 0, tree lane 0, producer)
+    // development profile (builds with -DTP_PH_PROF only; tools/prof_phase.py): this thread's
+    // cycle counters (warp 0 lane 0, tree lane 0, producer) and a per-CTA globaltimer timeline at
+    // prof[16 + 5 c + {start, pass-1 end, stats seen, tree end, end}]
+#ifdef TP_PH_PROF
     const bool prof = a.prof != nullptr && lane == 0 && (warp == 0 || warp == kPhTree || warp == kPhProducer);
+    unsigned long long* tl = a.prof ? a.prof + 16 + 5 * blockIdx.x : nullptr;
+#else
+    constexpr bool prof = false;
+    constexpr unsigned long long* tl = nullptr;
+#endif
     unsigned long long pc[16] = {};
     const unsigned long long p_start = prof ? clock64() : 0ull;
-    // timeline (development): globaltimer per CTA at prof[16 + 5 c + {start, pass-1 end, stats seen,
-    // tree end, end}]
-    unsigned long long* tl = a.prof ? a.prof + 16 + 5 * blockIdx.x : nullptr;
     if (tl && threadIdx.x == 0) tl[0] = globaltimer_ns();
     unsigned long long p_t = p_start;
     auto lap = [&](int slot) {

@@ -1,6 +1,8 @@
 """Per-role cycle breakdown of the phase kernel (development tool; tp_rowph.cu PhProf slots).
 
     python tools/prof_phase.py c3 [--reps 5]
+
+Builds (once) and loads paper_2001_04438_b200/libtwopass_prof.so, compiled with -DTP_PH_PROF.
 """
 import argparse
 import json
@@ -10,7 +12,12 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2001_04438_b200 import build as _build  # noqa: E402
+os.environ["TP_LIBRARY"] = _build.build(out=os.path.join(ROOT, "paper_2001_04438_b200", "libtwopass_prof.so"),
+                                        defines=("TP_PH_PROF",), force=not os.path.exists(
+                                            os.path.join(ROOT, "paper_2001_04438_b200", "libtwopass_prof.so")))
 import paper_2001_04438_b200 as tp  # noqa: E402
 import workloads  # noqa: E402
 
