@@ -62,6 +62,22 @@ __device__ __forceinline__ void load_stage(const In* stage, BlockVals& r, int ti
     }
 }
 
+// This thread's values of logical warp (8 h + wl) from half-stage `half` (a half-stage holds one contiguous half of a block: the values of logical warps 8 h .. 8 h + 7).
+template <typename In>
+__device__ __forceinline__ void load_half(const In* half, int wl, int lane, BlockVals& r) {
+    constexpr int V = InTraits<In>::V, NV = kPerThread / V;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int e = vec_off<V>(32 * wl + lane, k);  // wl < 8: offset within the half
+        if constexpr (V == 4) {
+            const float4 a = *reinterpret_cast<const float4*>(half + e);
+            r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
+        } else {
+            unpack_bf16x8(*reinterpret_cast<const uint4*>(half + e), &r.v[8 * k]);
+        }
+    }
+}
+
 // From global memory.  `vec`: 16-byte aligned rows (128-bit loads); otherwise scalar loads.
 // Elements past `valid` read as 0 (callers mask).  `last` = evict-first L2 policy.
 template <typename In>
@@ -297,13 +313,44 @@ __device__ __forceinline__ float block_tree_warps_sum(const float* w) {
     return t[0];
 }
 
-// Pass 1 of this warp's share of a block: warp pair in lane 0, returns the clamp decision.
+// ---- warp value of a block's thread pairs (reading G8): maximum first, then a sum tree.
+// The 32 thread pairs (m_t, n_t) of a warp combine to (M, N): N = max_t n_t, M = the perfect
+// binary tree of correctly rounded additions, in lane order, of m_t 2^(n_t - N) (exact power-of-two
+// scalings, flushed to 0 below 2^-126 as every 2^k of the path, reading G5).  This is Alg. 3's
+// max-exponent rescaling applied to the whole warp at once: where no scaled
+// value is subnormal it is bit for bit the perfect tree of pair merges over the same leaves
+// (scaling by 2^(n_node - N) commutes with each rounding), and it costs one integer max
+// (REDUX) and a tree of additions instead of a tree of merges (shuffles of m and n, two 2^k per
+// level).  Every kernel forms warp values with these functions, so all stay bit-identical.
+//
+// Key of a thread pair: the bits of n + 1.5*2^23, i.e. bits(1.5*2^23) + n for the integer n
+// (|n| <= 3025526 after the clamp decision, reading G11), so keys order like exponents; 0 for a
+// thread without elements (n = -FLT_MAX).
+__device__ __forceinline__ int pair_key(Pair p) {
+    return p.n > -4194304.0f ? __float_as_int(__fadd_rn(p.n, kMagic)) : 0;
+}
+// m 2^(n - N) for the warp's key kw (2^(key - kw), flushed to 0 for key - kw <= -127)
+__device__ __forceinline__ float pair_scaled(Pair p, int key, int kw) {
+    return __fmul_rn(p.m, pow2_bits(key - kw + 127));
+}
+// (M, N) from the sum and the warp's key; no element in the warp: (0, -FLT_MAX) like accv_pair
+__device__ __forceinline__ Pair warp_value_pair(float msum, int kw) {
+    return Pair{msum, kw ? __fsub_rn(__int_as_float(kw), kMagic) : -kFltMax};
+}
+// The warp value of this lane's thread pair and the 31 others; result in lane 0.
+__device__ __forceinline__ Pair warp_value(Pair p) {
+    const int key = pair_key(p);
+    const int kw = (int)__reduce_max_sync(0xffffffffu, (unsigned)key);
+    return warp_value_pair(warp_tree_sum(pair_scaled(p, key, kw)), kw);
+}
+
+// Pass 1 of this warp's share of a block: warp value in lane 0, returns the clamp decision.
 template <int V>
 __device__ __forceinline__ bool warp_pass1(const BlockVals& r, int valid, Pair* wp) {
     Pair acc = valid == kBlockElems ? pass1_thread<V, true, false>(r, valid) : pass1_thread<V, false, false>(r, valid);
     const bool clamped = __any_sync(0xffffffffu, acc_out_of_domain(acc));
     if (clamped) acc = pass1_thread<V, false, true>(r, valid);
-    *wp = warp_tree_pairs(acc);
+    *wp = warp_value(acc);
     return clamped;
 }
 

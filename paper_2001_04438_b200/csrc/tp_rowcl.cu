@@ -55,22 +55,6 @@ template <typename In> struct ClRing {
     static constexpr int S2 = (192 * 1024) / (kHalfElems * (int)sizeof(In));
 };
 
-// This thread's values of logical warp (8 h + wl) from half-stage `half` (see ClRing).
-template <typename In>
-__device__ __forceinline__ void load_half(const In* half, int wl, int lane, BlockVals& r) {
-    constexpr int V = InTraits<In>::V, NV = kPerThread / V;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const int e = vec_off<V>(32 * wl + lane, k);  // wl < 8: offset within the half
-        if constexpr (V == 4) {
-            const float4 a = *reinterpret_cast<const float4*>(half + e);
-            r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
-        } else {
-            unpack_bf16x8(*reinterpret_cast<const uint4*>(half + e), &r.v[8 * k]);
-        }
-    }
-}
-
 enum ClOp : int { kClP1 = 0, kClP2 = 2, kClExit = 4 };
 enum ClFlag : int { kClFirstP2 = 2 };
 // development counters (KArgs::prof): clock cycles summed over CTAs
@@ -343,9 +327,10 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     }
     if (warp == kWarps + 1) {
         // =============================================================== tree warp
-        // Per pass-1 block, in command order: the perfect tree over the 512 thread pairs in
-        // thread order (lane l reduces threads 16l..16l+15, then the warp tree) = the stream
-        // kernel's warp trees followed by its block tree over the 16 warps (reading G8).  After
+        // Per pass-1 block, in command order: the 16 warp values of the 512 thread pairs (lanes
+        // 2w, 2w + 1 hold warp w's threads 0-15 / 16-31: the warp's maximum key, its perfect
+        // sum tree as two 16-leaf subtrees and their sum, = warp_value of the other kernels),
+        // then the block tree over the 16 warps (reading G8).  After
         // a row's last local block: block values to every CTA of the cluster, then the row
         // statistics for this CTA's compute warps.
         long long p = 0;
@@ -361,13 +346,28 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 const int sl = (int)(p % T);
                 if (!wait_or_abort(&tp_full[sl], (uint32_t)((p / T) & 1), err, 512u)) { ok = false; break; }
                 const Pair* tq = tpairs[sl] + lane * 16;
-                const Pair t = tree_pairs_n<16>([&](int i) { return tq[i]; });
+                int key[16], kw = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    key[i] = pair_key(tq[i]);
+                    kw = max(kw, key[i]);
+                }
+                kw = max(kw, __shfl_xor_sync(0xffffffffu, kw, 1));  // the warp's maximum key
+                float sm[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) sm[i] = pair_scaled(tq[i], key[i], kw);
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1)
+#pragma unroll
+                    for (int i = 0; i + o < 16; i += 2 * o) sm[i] = __fadd_rn(sm[i], sm[i + o]);
+                const float msum = __fadd_rn(sm[0], __shfl_xor_sync(0xffffffffu, sm[0], 1));  // commutative
+                const Pair t = (lane & 1) ? pair_identity() : warp_value_pair(msum, kw);
                 unsigned m = 0;
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) m |= (unsigned)cbits[sl][w] << w;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tp_empty[sl]);
-                const Pair b = warp_tree_pairs(t);  // lane 0
+                const Pair b = warp_tree_pairs(t);  // lane 0: the 16 warps' tree (merges with identities are exact)
                 const float bm = __shfl_sync(0xffffffffu, b.m, 0), bn = __shfl_sync(0xffffffffu, b.n, 0);
                 if (lane == li) {
                     lval = make_float2(bm, bn);

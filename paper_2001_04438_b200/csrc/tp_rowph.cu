@@ -50,11 +50,23 @@ constexpr unsigned long long kPhChunk = TP_PH_CHUNK;  // items per queue claim
 // half frees as soon as its own 8 warps have read it: 6 x 32 KB fp32 / 12 x 16 KB bf16 = 192 KB.
 // (An odd H, 7 x 32 KB, would hold more bytes in flight, but then one half-stage serves both
 // halves in turn and the halves must stay in lockstep: measured 20% slower.)
+#ifndef TP_PH_H32
+#define TP_PH_H32 6
+#endif
 template <typename In> struct PhRing {
     static constexpr int kHalf = kBlockElems / 2;
-    static constexpr int H = sizeof(In) == 4 ? 6 : 12;
-    static_assert(H % 2 == 0, "a half-stage must serve one half");
+    static constexpr int H = sizeof(In) == 4 ? TP_PH_H32 : 2 * TP_PH_H32;
 };
+
+// Full barriers are per (half-stage, half of the block): with an odd number H of half-stages a
+// half-stage holds first and second halves in turn, and a warp of one half could otherwise test
+// the barrier two phases ahead of the other half's pending use (a parity wait cannot tell phase p
+// from p - 2).  Use u = 2 k + half of half-stage u mod H is the ph_use(u)-th of its barrier.
+template <int H>
+__device__ __forceinline__ long long ph_use(long long u) {
+    const long long p = u / H;  // uses of the half-stage before this one
+    return (H & 1) ? p >> 1 : p;
+}
 
 // Item `item` of the launch: pass-1 items [0, rows nb) row-major, then pass-2 items (blocks of a
 // row backwards).  A partial launch has only the first kind, a finish launch only the second.
@@ -106,7 +118,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     __shared__ long long slot_item[T];  // pass-1 item of a slot, -1 = end
     __shared__ long long meta[H];       // item of a half-stage use, -1 = end
     __shared__ Item meta_it[H];         // ... decoded (the producer decodes once per block)
-    __shared__ __align__(8) uint64_t full_bar[H];
+    __shared__ __align__(8) uint64_t full_bar[H][2];  // [half-stage][half of the block it holds]
     __shared__ __align__(8) uint64_t empty_bar[H];
     __shared__ __align__(8) uint64_t tfull[T];
     __shared__ __align__(8) uint64_t tempty[T];
@@ -123,7 +135,8 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     if (threadIdx.x == 0) {
         s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
         for (int h = 0; h < H; ++h) {
-            mbar_init(&full_bar[h], 1);
+            mbar_init(&full_bar[h][0], 1);
+            mbar_init(&full_bar[h][1], 1);
             mbar_init(&empty_bar[h], kPhCompute / 2);  // the 8 warps of the half
         }
         for (int t = 0; t < T; ++t) {
@@ -192,13 +205,13 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                     meta[h] = item >= total ? -1 : item;  // end mark in both halves
                     meta_it[h] = it;
                     if (n <= 0) {  // nothing to copy (end mark, or a short last block's 2nd half)
-                        mbar_arrive(&full_bar[h]);
+                        mbar_arrive(&full_bar[h][j]);
                         continue;
                     }
                     fence_proxy_async_smem();
-                    mbar_arrive_expect_tx(&full_bar[h], (uint32_t)n * (uint32_t)sizeof(In));
+                    mbar_arrive_expect_tx(&full_bar[h][j], (uint32_t)n * (uint32_t)sizeof(In));
                     tma_load_1d(stages + (size_t)h * HE, src + j * HE, (uint32_t)n * (uint32_t)sizeof(In),
-                                &full_bar[h], pol);
+                                &full_bar[h][j], pol);
                 }
                 if (item >= total) break;
             }
@@ -258,18 +271,18 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
         bool p1_done = false;
         float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
         const int half = warp >= kWarps / 2 ? 1 : 0;  // the half of every block this warp reads
+        bool fail = false;
         for (long long k = 0;; ++k) {
             const long long u = 2 * k + half;
             const int h = (int)(u % H);
             lap(kPhP2Work);
-            if (!wait_or_abort(&full_bar[h], (uint32_t)((u / H) & 1), err, 4u)) break;
+            if (!wait_or_abort(&full_bar[h][half], (uint32_t)(ph_use<H>(u) & 1), err, 4u)) { fail = true; break; }
             const long long item = meta[h];
             if (item < 0) break;  // end mark
             const Item it = meta_it[h];
             const int valid = (int)min((int64_t)kBlockElems, a.cols - it.blk * kBlockElems);
             BlockVals v;
-            // the canonical layout addresses the whole block (second half at +HE): rebase
-            load_stage<In>(stages + (size_t)h * HE - (size_t)half * HE, v);
+            load_half<In>(stages + (size_t)h * HE, warp & 7, lane, v);  // this warp's values of its half
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[h]);  // the half-stage can be refilled
             if (it.phase == 0) {  // pass 1
@@ -278,7 +291,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                 const bool clamped = warp_pass1<V>(v, valid, &wp);
                 const int t = (int)(ks % T);
                 lap(kPhP1Work);
-                if (ks >= T && !wait_or_abort(&tempty[t], (uint32_t)(((ks / T) - 1) & 1), err, 16u)) break;
+                if (ks >= T && !wait_or_abort(&tempty[t], (uint32_t)(((ks / T) - 1) & 1), err, 16u)) { fail = true; break; }
                 lap(kPhP1Slot);
                 if (lane == 0) {
                     wpairs[t][warp] = wp;
@@ -314,7 +327,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
             op_pass2<V>(v, st, ((mask >> warp) & 1u) != 0, a.y + it.row * a.cols + it.blk * kBlockElems, valid, true);
         }
         // end mark for the tree warp (its loop stops at the first slot holding -1)
-        if (A != kFinish) {
+        if (A != kFinish && !fail) {
             const int t = (int)(ks % T);
             if (!(ks >= T && !wait_or_abort(&tempty[t], (uint32_t)(((ks / T) - 1) & 1), err, 16u))) {
                 if (warp == 0 && lane == 0) slot_item[t] = -1;
