@@ -38,7 +38,10 @@ constexpr int kPhCompute = kWarps;         // 16 compute warps
 constexpr int kPhProducer = kWarps;        // warp 16
 constexpr int kPhTree = kWarps + 1;        // warp 17
 constexpr int kPhThreads = (kWarps + 2) * 32;
-constexpr int kPhSlots = 8;                // warp-pair slots between the compute warps and the tree warp
+#ifndef TP_PH_SLOTS
+#define TP_PH_SLOTS 16
+#endif
+constexpr int kPhSlots = TP_PH_SLOTS;      // warp-pair slots between the compute warps and the tree warp (<= 32)
 constexpr int64_t kPhMaxRows = 8;          // Two-Pass: rows of one launch (pass 2 waits for whole rows)
 #ifndef TP_PH_CHUNK
 #define TP_PH_CHUNK 2
@@ -61,12 +64,8 @@ template <typename In> struct PhRing {
 // Full barriers are per (half-stage, half of the block): with an odd number H of half-stages a
 // half-stage holds first and second halves in turn, and a warp of one half could otherwise test
 // the barrier two phases ahead of the other half's pending use (a parity wait cannot tell phase p
-// from p - 2).  Use u = 2 k + half of half-stage u mod H is the ph_use(u)-th of its barrier.
-template <int H>
-__device__ __forceinline__ long long ph_use(long long u) {
-    const long long p = u / H;  // uses of the half-stage before this one
-    return (H & 1) ? p >> 1 : p;
-}
+// from p - 2).  Use p of a half-stage (p = u / H for u = 2 k + half) is then use p / 2 of its
+// barrier (H odd), or use p (H even: a half-stage always holds the same half).
 
 // Item `item` of the launch: pass-1 items [0, rows nb) row-major, then pass-2 items (blocks of a
 // row backwards).  A partial launch has only the first kind, a finish launch only the second.
@@ -77,26 +76,10 @@ __device__ __forceinline__ Item ph_decode(const KArgs& a, int64_t item) {
     Item it;
     it.phase = A == kFinish ? 1 : (i >= n ? 1 : 0);
     const uint32_t g = (A == kTwoPass && i >= n) ? i - n : i;
-    const uint32_t r = g / nb, b = g - r * nb;
+    const uint32_t r = a.rows == 1 ? 0u : g / nb, b = g - r * nb;  // one row (C3, C5, chunks): no division
     it.row = r;
     it.blk = it.phase == 0 ? b : nb - 1 - b;
     return it;
-}
-
-// The block value (one whole warp) from its 16 warp pairs, bit-identical to block_tree_warps
-// (perfect tree over the warps in order; reading G8): lane w < 16 holds warp w's pair, lanes
-// 2o apart merge at level o.  Result in lane 0.
-__device__ __forceinline__ Pair ph_block_tree(const Pair* wp) {
-    const int lane = threadIdx.x & 31;
-    Pair v = lane < kWarps ? wp[lane] : pair_identity();
-#pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-        Pair r;
-        r.m = __shfl_down_sync(0xffffffffu, v.m, o);
-        r.n = __shfl_down_sync(0xffffffffu, v.n, o);
-        if ((lane & (2 * o - 1)) == 0) v = pair_merge(v, r);
-    }
-    return v;
 }
 
 // Development (KArgs::prof, tools/prof_phase.py): per-role clock cycles summed over CTAs.
@@ -113,8 +96,8 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     constexpr int HE = PhRing<In>::kHalf;     // elements per half-stage
     constexpr int T = kPhSlots;
     extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ __align__(16) Pair wpairs[T][kWarps];
-    __shared__ unsigned char cbits[T][kWarps];
+    __shared__ __align__(16) Pair wpairs[T][kWarps + 1];  // padded: the tree warp's lanes read different slots
+    __shared__ __align__(16) unsigned char cbits[T][kWarps];
     __shared__ long long slot_item[T];  // pass-1 item of a slot, -1 = end
     __shared__ long long meta[H];       // item of a half-stage use, -1 = end
     __shared__ Item meta_it[H];         // ... decoded (the producer decodes once per block)
@@ -179,11 +162,13 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
             unsigned long long next = atomicAdd(&hdr->counter, kPhChunk);
             unsigned long long end = next + kPhChunk;
             unsigned long long ahead = atomicAdd(&hdr->counter, kPhChunk);  // used one chunk later
-            for (long long k = 0;; ++k) {  // block k: half-stages 2k, 2k + 1 of the ring
+            // ring position of the next half-stage use: half-stage hs, its use number ps (32-bit
+            // counters advanced incrementally: no division in the loop)
+            int hs = 0;
+            uint32_t ps = 0;
+            for (;;) {  // one block: its two halves into the next two half-stage uses
                 lap(kPhProdTotal);
-                const long long u0 = 2 * k;
-                const int h0 = (int)(u0 % H);
-                if (u0 >= H && !wait_or_abort(&empty_bar[h0], (uint32_t)(((u0 / H) - 1) & 1), err, 64u)) break;
+                if (ps > 0 && !wait_or_abort(&empty_bar[hs], (ps - 1) & 1u, err, 64u)) break;
                 lap(kPhProdWait);
                 if (next == end) {
                     next = ahead;
@@ -196,11 +181,14 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                 const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
                 const In* src = x + it.row * a.cols + e0;
                 const uint64_t pol = it.phase == 0 ? pol_keep : pol_drop;
+                bool ok = true;
                 for (int j = 0; j < 2; ++j) {
-                    const long long u = u0 + j;
-                    const int h = (int)(u % H);
-                    if (j == 1 && u >= H && !wait_or_abort(&empty_bar[h], (uint32_t)(((u / H) - 1) & 1), err, 64u))
+                    const int h = hs;
+                    if (j == 1 && ps > 0 && !wait_or_abort(&empty_bar[h], (ps - 1) & 1u, err, 64u)) {
+                        ok = false;
                         break;
+                    }
+                    if (++hs == H) hs = 0, ++ps;
                     const int n = item >= total ? 0 : min(HE, valid - j * HE);
                     meta[h] = item >= total ? -1 : item;  // end mark in both halves
                     meta_it[h] = it;
@@ -208,12 +196,13 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                         mbar_arrive(&full_bar[h][j]);
                         continue;
                     }
-                    fence_proxy_async_smem();
+                    // (no proxy fence: the half-stage's previous contents were only read, and
+                    // those reads are ordered before this copy by the empty barrier)
                     mbar_arrive_expect_tx(&full_bar[h][j], (uint32_t)n * (uint32_t)sizeof(In));
                     tma_load_1d(stages + (size_t)h * HE, src + j * HE, (uint32_t)n * (uint32_t)sizeof(In),
                                 &full_bar[h][j], pol);
                 }
-                if (item >= total) break;
+                if (!ok || item >= total) break;
             }
             if (ahead == ~0ull) hdr->error |= 2u;  // consume the prefetched claim before leaving
         }
@@ -234,18 +223,18 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
             const long long my_item = lane < n ? slot_item[(k + lane) % T] : -1;
             const unsigned stop = __ballot_sync(0xffffffffu, lane < n && my_item < 0);
             const int m = stop ? __ffs(stop) - 1 : n;  // slots before the end mark
+            // lane j forms block k + j's value (all the batch's blocks at once): the perfect tree
+            // over its 16 warp values (reading G8) and its per-warp clamp mask
             float2 val = make_float2(0.f, 0.f);
             unsigned mask = 0;
-            for (int j = 0; j < m; ++j) {
-                const int t = (int)((k + j) % T);
-                const Pair bv = ph_block_tree(wpairs[t]);
-                const unsigned cb = lane < kWarps ? (unsigned)cbits[t][lane] : 0u;
-                const unsigned mm = __ballot_sync(0xffffffffu, cb != 0) & ((1u << kWarps) - 1u);
-                const float bm = __shfl_sync(0xffffffffu, bv.m, 0), bn = __shfl_sync(0xffffffffu, bv.n, 0);
-                if (lane == j) {
-                    val = make_float2(bm, bn);
-                    mask = mm;
-                }
+            if (lane < m) {
+                const int t = (int)((k + lane) % T);
+                const Pair bv = block_tree_warps(wpairs[t]);
+                val = make_float2(bv.m, bv.n);
+                const uint4 cb = *reinterpret_cast<const uint4*>(cbits[t]);
+                const unsigned w4[4] = {cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) mask |= ((w4[w >> 2] >> (8 * (w & 3))) & 0xffu) ? 1u << w : 0u;
             }
             __syncwarp();
             if (lane < m) mbar_arrive(&tempty[(k + lane) % T]);  // the slots are free again
@@ -272,11 +261,12 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
         float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
         const int half = warp >= kWarps / 2 ? 1 : 0;  // the half of every block this warp reads
         bool fail = false;
-        for (long long k = 0;; ++k) {
-            const long long u = 2 * k + half;
-            const int h = (int)(u % H);
+        int h = half;   // half-stage of this warp's next use (u = 2 k + half), incrementally
+        uint32_t pu = 0;  // ... and that half-stage's use number u / H
+        for (;; h += 2) {
+            if (h >= H) h -= H, ++pu;
             lap(kPhP2Work);
-            if (!wait_or_abort(&full_bar[h][half], (uint32_t)(ph_use<H>(u) & 1), err, 4u)) { fail = true; break; }
+            if (!wait_or_abort(&full_bar[h][half], ((H & 1) ? pu >> 1 : pu) & 1u, err, 4u)) { fail = true; break; }
             const long long item = meta[h];
             if (item < 0) break;  // end mark
             const Item it = meta_it[h];
