@@ -161,16 +161,17 @@ __device__ void retire_batch(const KArgs& a, bool mine, const Item& it, float2 v
     unsigned* rt = reinterpret_cast<unsigned*>(a.ws + a.lay.row_tickets);
     unsigned* row_clamp = reinterpret_cast<unsigned*>(a.ws + a.lay.row_clamp);
     const int64_t g = it.blk / kGroupBlocks;
-    if (mine) block_vals[it.row * a.nb + it.blk] = val;
-    __threadfence();
     bool last = false;
     if (mine) {
+        block_vals[it.row * a.nb + it.blk] = val;
         const int64_t gsize = min((int64_t)kGroupBlocks, a.nb - g * kGroupBlocks);
-        last = atomicAdd(&gt[it.row * a.ng + g], 1u) == (unsigned)(gsize - 1);
+        // release: this lane's block value before its ticket; acquire: the group's last ticket
+        // sees every other block value of the group (their tickets released them)
+        last = atom_add_acq_rel_gpu(&gt[it.row * a.ng + g], 1u) == (unsigned)(gsize - 1);
     }
     unsigned fin = __ballot_sync(0xffffffffu, last);
     if (!fin) return;
-    __threadfence();
+    __syncwarp();  // the acquiring lanes' view passes to the whole warp (warp barrier orders memory)
     while (fin) {
         const int l = __ffs(fin) - 1;
         fin &= fin - 1;
@@ -186,11 +187,10 @@ __device__ void retire_batch(const KArgs& a, bool mine, const Item& it, float2 v
         if (lane == 0) {
             gt[row * a.ng + gg] = 0u;  // ticket reset for the next phase / launch
             group_vals[row * a.ng + gg] = gres;
-            __threadfence();
-            rlast = atomicAdd(&rt[row], 1u) == (unsigned)(a.ng - 1);
+            rlast = atom_add_acq_rel_gpu(&rt[row], 1u) == (unsigned)(a.ng - 1);
         }
         if (!__shfl_sync(0xffffffffu, rlast, 0)) continue;
-        __threadfence();
+        __syncwarp();
         const float2* rv = group_vals + row * a.ng;
         const float2 root = warp_reduce_leaves(kind, a.ng, [&](int64_t j) { return __ldcg(rv + j); });
         if (lane == 0) {

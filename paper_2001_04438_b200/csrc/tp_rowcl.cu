@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             const unsigned parity = (use_par >> s) & 1u;
             use_par ^= 1u << s;
             busy |= 1u << s;
-            fence_proxy_async_smem();
+            // (no proxy fence: the stage's previous contents were only read, and those reads are
+            // ordered before this copy by its empty barrier)
             mbar_arrive_expect_tx(&full_bar[s], bytes);
             if (n > 0) {
                 In* dst = stages + (size_t)s * HE;

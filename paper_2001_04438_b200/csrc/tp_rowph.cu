@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     const unsigned want = s_epoch + 1u;
     // development profile (builds with -DTP_PH_PROF only; tools/prof_phase.py): this thread's
     // cycle counters (warp 0 lane 0, tree lane 0, producer) and a per-CTA globaltimer timeline at
-    // prof[16 + 5 c + {start, pass-1 end, stats seen, tree end, end}]
+    // prof[16 + 5 c + {start, pass-1 end, stats seen, last retirement, end}]
 #ifdef TP_PH_PROF
     const bool prof = a.prof != nullptr && lane == 0 && (warp == 0 || warp == kPhTree || warp == kPhProducer);
     unsigned long long* tl = a.prof ? a.prof + 16 + 5 * blockIdx.x : nullptr;
@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                 if (mask) atomicOr(reinterpret_cast<unsigned*>(a.ws + a.lay.row_clamp) + it.row, 1u);
             }
             retire_batch<A == kFinish ? kTwoPass : A>(a, mine, it, val, 0.0f, want);
+            if (tl && lane == 0 && m > 0) tl[3] = globaltimer_ns();  // development timeline: last retirement
             lap(kPhTreeRetire);
             pc[kPhTreeBatches] += 1;
             pc[kPhTreeBlocks] += (unsigned long long)m;
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                     if (lane == 0) ok = wait_flag(row_ready + it.row * 2, want, err);
                     if (!__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) break;
                     st = __ldcg(reinterpret_cast<const float4*>(a.ws + a.lay.row_stats) + it.row * 2);
-                    if (tl && threadIdx.x == 0 && tl[2] == 0) tl[2] = globaltimer_ns();
+                    if (tl && threadIdx.x == 0) tl[2] = globaltimer_ns();
                 }
                 cur_row = it.row;
             }
@@ -326,7 +327,6 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
             }
         }
     }
-    if (tl && warp == kPhTree && lane == 0) tl[3] = globaltimer_ns();
     if (prof) {
         lap(warp == 0 ? kPhP2Work : warp == kPhTree ? kPhTreeRetire : kPhProdTotal);
         const int tot = warp == 0 ? kPhComputeTotal : warp == kPhTree ? kPhTreeTotal : kPhProdTotal;

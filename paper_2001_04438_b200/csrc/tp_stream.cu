@@ -268,7 +268,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const KArgs a
                                                          : ((P > 1 && it.phase < P - 1) || A == kPartial));
                 In* dst = stages + (size_t)s * kBlockElems;
                 const unsigned long long f0 = a.prof ? clock64() : 0ull;
-                fence_proxy_async_smem();
+                // (no proxy fence: the stage's previous contents were only read, and those reads
+                // are ordered before this copy by its empty barrier)
                 const unsigned long long f1 = a.prof ? clock64() : 0ull;
                 mbar_arrive_expect_tx(&full_bar[s], bytes);
                 if (a.l2_hints) tma_load_1d(dst, x + it.row * a.cols + e0, bytes, &full_bar[s], keep ? pol_keep : pol_drop);

@@ -55,8 +55,8 @@ def main():
         tl = np.zeros((1, 5), dtype=np.int64)
     t0 = tl[:, 0].min()
     rel = (tl - t0) / 1e3
-    print("timeline us (min / median / max over CTAs): start, pass-1 end, stats seen, tree end, end")
-    for i, nm in enumerate(["start", "p1_end", "stats", "tree_end", "end"]):
+    print("timeline us (min / median / max over CTAs): start, pass-1 end, stats seen, last retirement, end")
+    for i, nm in enumerate(["start", "p1_end", "stats", "retired", "end"]):
         col = rel[:, i][tl[:, i] > 0]
         if col.size:
             print(f"  {nm:9s} {col.min():9.1f} {np.median(col):9.1f} {col.max():9.1f}")

@@ -19,7 +19,7 @@ import paper_2001_04438_b200 as tp  # noqa: E402
 import workloads  # noqa: E402
 from gpu_helpers import assert_parity  # noqa: E402
 
-SCHEDS = [tp.SCHED_AUTO, tp.SCHED_CLUSTER, tp.SCHED_SMALL, tp.SCHED_HOLD]
+SCHEDS = [tp.SCHED_AUTO, tp.SCHED_CLUSTER, tp.SCHED_SMALL, tp.SCHED_HOLD, tp.SCHED_PHASE]
 
 
 def main():
