@@ -284,7 +284,11 @@ int softmax_watchdog_flags(const void* workspace, int reset);
  *           (out0 = m, out1 = n)
  *        7: the kernels' integer-pipe 2^k: out0 = 2^(d - 127) for d = round(a) <= 254,
  *           +0 for d <= 0 (the scale of Alg. 3's accumulate and pass 2, PAPER.md:161, 168,
- *           flushed below 2^-126 per PAPER.md:252-258) */
+ *           flushed below 2^-126 per PAPER.md:252-258)
+ *        8: warp value of thread pairs (a[2i], a[2i+1]), i = thread, count a multiple of 32:
+ *           per warp w, out0[32 w + 0..3] = (M, N) of the kernels' max-first warp value and
+ *           (m, n) of the perfect tree of pair merges over the same 32 pairs in lane order
+ *           (reading G8; the two agree outside the sub-2^-126 band) */
 int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                 cudaStream_t stream);
 

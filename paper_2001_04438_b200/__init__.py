@@ -353,7 +353,7 @@ def watchdog_flags(workspace: torch.Tensor | None = None, reset: bool = True) ->
 def debug_op(what: int, a: torch.Tensor, b: torch.Tensor | None = None):
     """Unit-test hook (include/twopass.h tp_debug_op)."""
     a = _prep(a.float())
-    count = a.numel() // 2 if what == 2 else a.numel()
+    count = a.numel() // 2 if what in (2, 8) else a.numel()
     o0 = torch.empty(count, dtype=torch.float32, device=a.device)
     o1 = torch.empty(count, dtype=torch.float32, device=a.device)
     bp = _prep(b.float()).data_ptr() if b is not None else None

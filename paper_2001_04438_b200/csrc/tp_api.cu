@@ -774,7 +774,8 @@ int tp_bench_compute(int what, int in_dtype, int64_t ctas, int reps, float* sink
 
 int tp_debug_op(int what, const float* a, const float* b, float* out0, float* out1, int64_t count,
                 cudaStream_t stream) {
-    if (count < 0 || what < 0 || what > 7 || (count > 0 && (!a || !out0))) return TP_EINVAL;
+    if (count < 0 || what < 0 || what > 8 || (count > 0 && (!a || !out0))) return TP_EINVAL;
+    if (what == 8 && count % 32 != 0) return TP_EINVAL;  // whole warps
     if ((what == 0 || what == 2 || what == 6) && count > 0 && !out1) return TP_EINVAL;
     if (what == 2 && count > 0 && !b) return TP_EINVAL;
     cudaError_t e = tp::launch_debug(what, a, b, out0, out1, count, stream);

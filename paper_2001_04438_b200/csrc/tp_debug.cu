@@ -7,6 +7,21 @@ namespace tp {
 
 __global__ void debug_kernel(int what, const float* a, const float* b, float* o0, float* o1, int64_t count) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (what == 8) {  // whole warps (count % 32 == 0, checked by the caller)
+        if (i - (threadIdx.x & 31) >= count) return;
+        const Pair p{a[2 * i], a[2 * i + 1]};
+        const Pair wv = warp_value(p), pt = warp_tree_pairs(p);  // both valid in lane 0
+        const int lane = threadIdx.x & 31;
+        const float r[4] = {wv.m, wv.n, pt.m, pt.n};
+        float mine = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float v = __shfl_sync(0xffffffffu, r[j], 0);
+            if (lane == j) mine = v;
+        }
+        if (lane < 4) o0[i] = mine;
+        return;
+    }
     if (i >= count) return;
     switch (what) {
         case 0: {

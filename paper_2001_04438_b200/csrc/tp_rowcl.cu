@@ -41,6 +41,15 @@ constexpr int kClMaxLocal = 32;          // blocks per CTA per row (lane of warp
 template <typename In> constexpr int kClMinLocal = sizeof(In) == 4 ? 2 : 4;
 constexpr int kClThreads = kThreads + 96;  // + producer A, tree warp, producer B
 constexpr int kClCmdSlots = 16;
+// Producer A's lead over producer B, in rows (pass 1 of row k starts once producer B has started
+// row k - kClLead), and the row-statistics slots between the tree warp and team B: the tree warp
+// can be at most kClLead rows ahead of team B's statistics wait (given the minimum share below),
+// so kClLead + 1 slots keep it from completing a slot's barrier twice ahead of team B.
+#ifndef TP_CL_LEAD
+#define TP_CL_LEAD 1
+#endif
+constexpr int kClLead = TP_CL_LEAD;
+constexpr int kClStSlots = kClLead + 1;
 constexpr int kClTeam = kWarps / 2;     // warps per compute team
 constexpr int kClTpSlots = 4;            // pass-1 thread-pair buffers between compute and tree warps
 
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     __shared__ __align__(16) Pair tpairs[T][kThreads];     // thread pairs of pass-1 blocks
     __shared__ unsigned char cbits[T][kWarps];            // per-warp clamp decisions of those blocks
     __shared__ __align__(16) float2 rowvals[2][kClMaxNb];  // written by every CTA of the cluster
-    __shared__ float4 row_st[2];                          // (n_sum - 1, 0.5 / m_sum, any local block clamped)
+    __shared__ float4 row_st[kClStSlots];                 // (n_sum - 1, 0.5 / m_sum, any local block clamped)
     __shared__ __align__(8) uint64_t full_bar[S];
     __shared__ __align__(8) uint64_t empty_bar[S];
     __shared__ __align__(8) uint64_t cfull_bar[2][C];
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     __shared__ __align__(8) uint64_t tp_full[T];           // count 8: thread pairs written
     __shared__ __align__(8) uint64_t tp_empty[T];          // count 1: read by the tree warp
     __shared__ __align__(8) uint64_t row_bar[2];           // count CL: one remote arrive per CTA
-    __shared__ __align__(8) uint64_t st_bar[2];            // count 1: row_st written
+    __shared__ __align__(8) uint64_t st_bar[kClStSlots];   // count 1: row_st written (slot k mod kClStSlots)
     __shared__ int p2_row;                                 // row iteration producer B has reached
 
     publish_abort_word(a);
@@ -187,10 +196,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             mbar_init(&tp_full[i], kClTeam);
             mbar_init(&tp_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&row_bar[i], CL);
-            mbar_init(&st_bar[i], 1);
-        }
+        for (int i = 0; i < 2; ++i) mbar_init(&row_bar[i], CL);
+        for (int i = 0; i < kClStSlots; ++i) mbar_init(&st_bar[i], 1);
         fence_mbar_init();
         p2_row = -1;
     }
@@ -393,8 +400,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             const float2 st = cl_row_stats(rowvals[par], nb);
             if (lane == 0) {
                 if (anyc) __threadfence_block();  // the block_clamp stores (all lanes) before the flag
-                row_st[par] = make_float4(st.x, st.y, anyc ? 1.0f : 0.0f, 0.0f);
-                mbar_arrive(&st_bar[par]);
+                row_st[k % kClStSlots] = make_float4(st.x, st.y, anyc ? 1.0f : 0.0f, 0.0f);
+                mbar_arrive(&st_bar[k % kClStSlots]);
             }
         }
         return;
@@ -432,7 +439,6 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         const int64_t row = cid + (int64_t)cmd.k * ncl;
         const int blk = cmd.li;  // absolute block index
         const int valid = (int)min((int64_t)kBlockElems, a.cols - (int64_t)blk * kBlockElems);
-        const int par = cmd.k & 1;
         // the block's two half-stages and their full-barrier parities (ClCmd::stage packing)
         const int st_pack = cmd.stage;
         BlockVals v;
@@ -463,8 +469,9 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             if (lane == 0) mbar_arrive(&tp_full[sl]);
         } else {
             if (cmd.flags & kClFirstP2) {  // the row's statistics, from the tree warp
-                if (!wait_or_abort(&st_bar[par], (uint32_t)((cmd.k >> 1) & 1), err, 256u)) break;
-                st = row_st[par];
+                const int ss = cmd.k % kClStSlots;
+                if (!wait_or_abort(&st_bar[ss], (uint32_t)((cmd.k / kClStSlots) & 1), err, 256u)) break;
+                st = row_st[ss];
                 lap(kProfRowWait);
             }
             const unsigned mask = st.z != 0.0f   // some local block of the row took the clamped path
@@ -663,7 +670,7 @@ cudaError_t launch_rowcl(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s) {
     // these values (the tree warp never laps team B's statistics barrier): no override.
     constexpr int S2 = ClRing<In>::S2;
     constexpr int SA = S2 / 2;
-    constexpr int LA = 1;
+    constexpr int LA = kClLead;
     static_assert(2 * kClMinLocal<In> > S2 - SA, "a share must exceed the pass-2 pool");
     last_plan() = Plan{3, kTwoPass, ncl * CL, CL, 0, SA};  // lookahead_rows: side rows (launch_split)
     if (a.prof) return cudaLaunchKernelEx(&cfg, rowcl_kernel<In, true>, a, CL, SA, LA);

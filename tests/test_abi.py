@@ -57,6 +57,13 @@ def test_host_only_entry_points_without_gpu(so):
     assert lib.softmax_workspace_bytes(256, 800000) > 256 * 49 * 8
     lib.softmax_status_str.restype = ctypes.c_char_p
     assert lib.softmax_status_str(1) == b"invalid argument"
+    # argument errors are decided on the host, before any CUDA call
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    lib.tp_debug_op.argtypes = [ctypes.c_int, vp, vp, vp, vp, i64, vp]
+    dummy = ctypes.c_void_p(16)
+    assert lib.tp_debug_op(9, dummy, None, dummy, dummy, 32, None) == 1   # unknown op
+    assert lib.tp_debug_op(8, dummy, None, dummy, dummy, 31, None) == 1   # warp value: whole warps only
+    assert lib.tp_debug_op(0, None, None, dummy, dummy, 4, None) == 1     # missing input
 
 
 def test_binding_fails_loudly_without_library(monkeypatch, tmp_path):

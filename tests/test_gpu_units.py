@@ -211,3 +211,45 @@ def test_hot_path_pow2_bits_exhaustive():
     got = tp.debug_op(7, torch.from_numpy(d).cuda())[0].cpu().numpy()
     want = np.array([np.float32(2.0 ** (int(k) - 127)) if k >= 1 else np.float32(0.0) for k in d], np.float32)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+# ------------------------------------------------------------------ warp value (tp_debug_op 8)
+
+def _warp_cases(nwarps, seed):
+    """Thread pairs like pass 1's accumulators: m in [sqrt(2)/2, 32 sqrt(2)], integer n around a
+    per-warp base with spreads from a few to thousands (the flush band at 126-127 included),
+    empty threads (0, -FLT_MAX), a few all-empty warps, and short mantissas (ties in the sums)."""
+    rng = np.random.default_rng(seed)
+    m = rng.uniform(0.70710678, 45.254834, size=(nwarps, 32)).astype(np.float32)
+    short = rng.random((nwarps, 32)) < 0.2
+    m[short] = (np.round(m[short] * 8) / 8).astype(np.float32)  # few significant bits
+    base = rng.integers(-3_000_000, 3_000_000, size=(nwarps, 1))
+    spread = rng.choice([3, 30, 120, 126, 127, 128, 140, 300, 3000], size=(nwarps, 1))
+    n = (base - rng.integers(0, spread + 1, size=(nwarps, 32))).astype(np.float32)
+    n[:, 0:1] = base  # one thread at the warp maximum
+    band = rng.random((nwarps, 32)) < 0.1  # exactly at the flush boundary of the warp maximum
+    n[band] = (base - rng.choice([125, 126, 127], size=(nwarps, 32)))[band]
+    empty = rng.random((nwarps, 32)) < 0.05
+    m[empty], n[empty] = 0.0, -np.float32(3.4028234663852886e38)
+    m[:4], n[:4] = 0.0, -np.float32(3.4028234663852886e38)  # all-empty warps
+    return m, n
+
+
+def test_warp_value_is_the_pair_merge_tree():
+    # reading G8: the kernels' warp value (maximum first, then a sum tree of the exactly rescaled
+    # mantissas) is the perfect tree of pair merges (Alg. 3's update, PAPER.md:160-162) over the
+    # same 32 thread pairs in lane order, bit for bit, including spreads across the 2^-126 flush
+    m, n = _warp_cases(20000, 21)
+    a = torch.from_numpy(np.stack([m, n], -1).reshape(-1)).cuda()
+    o = tp.debug_op(8, a)[0].cpu().numpy().reshape(-1, 32)[:, :4]
+    assert np.array_equal(o[:, 0].view(np.uint32), o[:, 2].view(np.uint32)), "M differs"
+    assert np.array_equal(o[:, 1], o[:, 3]), "N differs"
+    # and against exact rationals: M 2^N within half an ulp per level of the 5-level tree
+    for w in range(4, 400):
+        nmax = int(n[w][m[w] > 0].max())
+        exact = sum(Fraction(float(mi)) * Fraction(2) ** (int(ni) - nmax) for mi, ni in zip(m[w], n[w])
+                    if mi > 0 and int(ni) - nmax >= -126)
+        assert o[w, 1] == nmax
+        rel = abs(Fraction(float(o[w, 0])) - exact) / exact
+        assert rel <= Fraction(5, 2 ** 24), (w, float(rel))
+    assert np.all(o[:4, 0] == 0.0) and np.all(o[:4, 1] == -np.float32(3.4028234663852886e38))
