@@ -71,6 +71,10 @@ template <typename In> struct PhRing {
 // row backwards).  A partial launch has only the first kind, a finish launch only the second.
 template <int A>
 __device__ __forceinline__ Item ph_decode(const KArgs& a, int64_t item) {
+    // Two-Pass over many rows (a.L > 0): the stream kernel's interleaved order, pass 1 of row
+    // s then pass 2 of row s - L in slot s (tp_sched.cuh decode_item), so a row's re-read
+    // follows its pass 1 by L rows and stays in L2
+    if (A == kTwoPass && a.L > 0) return decode_item<kTwoPass>(item, a.rows, a.nb, a.L);
     // 32-bit arithmetic: a launch has far fewer than 2^31 blocks (2^31 blocks = 2^45 elements)
     const uint32_t n = (uint32_t)(a.rows * a.nb), nb = (uint32_t)a.nb, i = (uint32_t)item;
     Item it;
@@ -340,6 +344,16 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     if (threadIdx.x == 0) exit_and_reset(hdr);
 }
 
+// Rows of lookahead for the interleaved order: the items claimed between a row's last pass-1
+// block and its released statistics (the ring, the tree warp's slots and the queue chunks of
+// every CTA) span about grid x 24 items, i.e. grid x 24 / (2 nb) slots.
+static int64_t ph_default_lookahead(int64_t nb, int64_t grid) {
+#ifndef TP_PH_LOOKAHEAD_ITEMS
+#define TP_PH_LOOKAHEAD_ITEMS 24
+#endif
+    return (grid * TP_PH_LOOKAHEAD_ITEMS + 2 * nb - 1) / (2 * nb) + 1;
+}
+
 template <typename In, int A>
 cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     int dev = 0;
@@ -364,7 +378,14 @@ cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s) {
     if (o.grid_ctas > 0 && o.grid_ctas < grid) grid = o.grid_ctas;
     if (grid > a.rows * a.nb) grid = a.rows * a.nb;
     a.total_items = a.rows * a.nb * (A == kTwoPass ? 2 : 1);
-    last_plan() = Plan{5, A, grid, 0, 0, PhRing<In>::H};
+    // interleaved rows (Two-Pass, more rows than kPhMaxRows or a requested lookahead): pass 2 of
+    // row r is taken L rows after its pass 1
+    a.L = 0;
+    if (A == kTwoPass && (a.rows > kPhMaxRows || o.lookahead_rows > 0)) {
+        const int64_t L = o.lookahead_rows > 0 ? o.lookahead_rows : ph_default_lookahead(a.nb, grid);
+        a.L = L < a.rows ? L : a.rows;
+    }
+    last_plan() = Plan{5, A, grid, 0, a.L, PhRing<In>::H};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kPhThreads);
