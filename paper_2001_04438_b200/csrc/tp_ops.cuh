@@ -191,8 +191,14 @@ __device__ void retire_batch(const KArgs& a, bool mine, const Item& it, float2 v
         }
         if (!__shfl_sync(0xffffffffu, rlast, 0)) continue;
         __syncwarp();
+#ifdef TP_PH_PROF  // development timeline (tools/prof_phase.py): the row tree's start and end
+        if (a.prof && lane == 0) a.prof[16 + 5 * 200] = globaltimer_ns();
+#endif
         const float2* rv = group_vals + row * a.ng;
         const float2 root = warp_reduce_leaves(kind, a.ng, [&](int64_t j) { return __ldcg(rv + j); });
+#ifdef TP_PH_PROF
+        if (a.prof && lane == 0) a.prof[16 + 5 * 200 + 1] = globaltimer_ns();
+#endif
         if (lane == 0) {
             rt[row] = 0u;
             float clamped = 0.0f;  // did any block of the row take the clamped path?

@@ -152,29 +152,76 @@ __device__ __forceinline__ int red_kind(int phase) {
 
 // Canonical warp-level reduction of n leaves (perfect tree over the padded power of two):
 // lane l reduces leaves [l*c, (l+1)*c) in order, then the 32 lane results are tree-reduced.
+// With c >= kLeafChunk a lane loads its leaves a chunk at a time with independent loads (a row
+// of 2048 groups would otherwise wait on 64 dependent L2 round trips per lane: ~40 us at the end
+// of C5's pass 1); each chunk's perfect subtree, then the chunks' perfect tree, is the perfect
+// tree over the c leaves.
+constexpr int kLeafChunk = 8;
 template <typename LeafFn>
 __device__ __forceinline__ float2 warp_reduce_leaves(int kind, int64_t n, LeafFn leaf) {
     const int lane = threadIdx.x & 31;
     const int64_t P = next_pow2(n);
     const int64_t c = P > 32 ? P / 32 : 1;
     const int64_t base = (int64_t)lane * c;
+    constexpr int K = kLeafChunk;
+    const float ninf = -__int_as_float(0x7f800000);
+    // chunk j of this lane's leaves (c >= K), positions past n hold `pad`
+    auto load_chunk = [&](int64_t j, float2 pad, float2 (&f)[K]) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int64_t q = base + j * K + i;
+            f[i] = q < n ? leaf(q) : pad;
+        }
+    };
     if (kind == kRedMax) {
-        float m = -__int_as_float(0x7f800000);
-        for (int64_t j = base; j < base + c && j < n; ++j) m = fmaxf(m, leaf(j).x);
+        float m = ninf;
+        if (c >= K) {
+            for (int64_t j = 0; j < c / K && base + j * K < n; ++j) {
+                float2 f[K];
+                load_chunk(j, make_float2(ninf, 0.0f), f);
+#pragma unroll
+                for (int i = 0; i < K; ++i) m = fmaxf(m, f[i].x);
+            }
+        } else {
+            for (int64_t j = base; j < base + c && j < n; ++j) m = fmaxf(m, leaf(j).x);
+        }
         return make_float2(warp_max(m), 0.0f);
     }
     if (kind == kRedSum) {
         float v = 0.0f;
-        if (base < n) v = seq_tree_sum((int)c, [&](int i) { return base + i < n ? leaf(base + i).x : 0.0f; });
+        if (base < n) {
+            if (c >= K) {
+                v = seq_tree_sum((int)(c / K), [&](int j) {
+                    float2 f[K];
+                    load_chunk(j, make_float2(0.0f, 0.0f), f);
+#pragma unroll
+                    for (int o = 1; o < K; o <<= 1)
+#pragma unroll
+                        for (int i = 0; i + o < K; i += 2 * o) f[i].x = __fadd_rn(f[i].x, f[i + o].x);
+                    return f[0].x;
+                });
+            } else {
+                v = seq_tree_sum((int)c, [&](int i) { return base + i < n ? leaf(base + i).x : 0.0f; });
+            }
+        }
         return make_float2(warp_tree_sum(v), 0.0f);
     }
     Pair v = pair_identity();
-    if (base < n)
-        v = seq_tree_pairs((int)c, [&](int i) {
-            if (base + i >= n) return pair_identity();
-            const float2 f = leaf(base + i);
-            return Pair{f.x, f.y};
-        });
+    if (base < n) {
+        if (c >= K) {
+            v = seq_tree_pairs((int)(c / K), [&](int j) {
+                float2 f[K];
+                load_chunk(j, make_float2(0.0f, ninf), f);  // (0, -inf): the identity
+                return tree_pairs_n<K>([&](int i) { return Pair{f[i].x, f[i].y}; });
+            });
+        } else {
+            v = seq_tree_pairs((int)c, [&](int i) {
+                if (base + i >= n) return pair_identity();
+                const float2 f = leaf(base + i);
+                return Pair{f.x, f.y};
+            });
+        }
+    }
     v = warp_tree_pairs(v);
     return make_float2(v.m, v.n);
 }
@@ -233,7 +280,7 @@ __device__ __forceinline__ bool wait_flag(const unsigned* f, unsigned want, unsi
     const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_gpu(f) != want) {
         __nanosleep(ns);
-        ns = ns < 1024 ? ns * 2 : ns;
+        ns = ns < 256 ? ns * 2 : ns;
         if (globaltimer_ns() - t0 > kWaitTimeoutNs) {  // never hang the GPU on a bug
             raise_abort(err, 1u);
             return false;

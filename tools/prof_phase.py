@@ -37,7 +37,7 @@ def main():
         torch.from_numpy(x).cuda()
     y = torch.empty(xd.shape, dtype=torch.float32, device="cuda")
     tp.softmax_ex(xd, out=y, schedule=tp.SCHED_PHASE)
-    buf = torch.zeros(16 + 5 * 200, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(16 + 5 * 200 + 8, dtype=torch.int64, device="cuda")
     tp.lib().tp_set_profile_buffer(buf.data_ptr())
     buf.zero_()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -48,7 +48,8 @@ def main():
     e.synchronize()
     tp.lib().tp_set_profile_buffer(None)
     c = buf.cpu().numpy().astype(np.float64)
-    tl = buf[16:].cpu().numpy().reshape(-1, 5)  # last launch's per-CTA timeline (ns)
+    rt = buf[16 + 5 * 200:16 + 5 * 200 + 2].cpu().numpy()  # the row tree's start / end (last launch)
+    tl = buf[16:16 + 5 * 200].cpu().numpy().reshape(-1, 5)  # last launch's per-CTA timeline (ns)
     tl = tl[tl[:, 0] > 0]
     if not tl.size:
         print("no timeline (counters only)", c[:16].tolist())
@@ -60,6 +61,8 @@ def main():
         col = rel[:, i][tl[:, i] > 0]
         if col.size:
             print(f"  {nm:9s} {col.min():9.1f} {np.median(col):9.1f} {col.max():9.1f}")
+    if rt[0] > 0:
+        print(f"  row tree  {(rt[0] - t0) / 1e3:9.1f} .. {(rt[1] - t0) / 1e3:9.1f}")
     if os.environ.get("PH_DUMP"):
         np.savetxt(os.environ["PH_DUMP"], rel, fmt="%.1f")
     ctas = max(c[15], 1)
