@@ -404,9 +404,14 @@ class Runner:
         if plan["kernel"] == "cluster" and plan["lookahead_rows"] > 0:
             launches_per_step += 1  # the tail rows' concurrent launch
         kernel_name = KERNEL_NAMES.get(plan["kernel"], plan["kernel"]).format(In="float" if dtype == "f32" else "uint16_t")
-        if chunked:
-            kernel_name = "tp::stream_kernel<{In},kPartial> + tp::stream_kernel<{In},kFinish>".format(
-                In="float" if dtype == "f32" else "uint16_t")
+        if chunked:  # the partial's and the finish's kernels (one untimed call each, after timing)
+            In = "float" if dtype == "f32" else "uint16_t"
+            names = {"phase": "tp::rowph_kernel<{In},{A}>", "stream": "tp::stream_kernel<{In},{A}>"}
+            tp.partial(x, workspace=pairs_ws)
+            kp = tp.last_plan()["kernel"]
+            kernel_name = (names.get(kp, kp).format(In=In, A="kPartial") + " + "
+                           + names.get(plan["kernel"], plan["kernel"]).format(In=In, A="kFinish"))
+            self.torch.cuda.synchronize(self.dev)
         if tp.watchdog_flags(ws, reset=True):
             raise RuntimeError("watchdog fired during the benchmark: results invalid")
 
@@ -543,10 +548,19 @@ def main():
     import torch.distributed as dist
     import workloads
 
+    # development only (functional check of the N > 1 code paths on a one-GPU box; not a
+    # measurement): TP_BENCH_ONE_DEVICE=1 puts every rank on cuda:0, TP_BENCH_BACKEND=gloo
+    # replaces NCCL, which refuses two ranks on one device
+    if os.environ.get("TP_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("TP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     if args.workload == "c5":  # M of the ties: one host scan on rank 0, broadcast (reading G16)
         v = [workloads.c5_tie_value() if rank == 0 else None]
         if world > 1:
