@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
     __shared__ __align__(8) uint64_t full_bar[H][2];  // [half-stage][half of the block it holds]
     __shared__ __align__(8) uint64_t empty_bar[H];
     __shared__ __align__(8) uint64_t tfull[T];
-    __shared__ __align__(8) uint64_t tempty[T];
+    __shared__ unsigned long long s_tree_done;  // slots the tree warp has consumed (monotonic)
     __shared__ unsigned s_epoch;
 
     pdl_wait_and_release();  // programmatic launch: the previous grid on the stream is complete
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
         }
         for (int t = 0; t < T; ++t) {
             mbar_init(&tfull[t], kPhCompute);
-            mbar_init(&tempty[t], 1);
+        s_tree_done = 0ull;
         }
         fence_mbar_init();
     }
@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                 for (int w = 0; w < kWarps; ++w) mask |= ((w4[w >> 2] >> (8 * (w & 3))) & 0xffu) ? 1u << w : 0u;
             }
             __syncwarp();
-            if (lane < m) mbar_arrive(&tempty[(k + lane) % T]);  // the slots are free again
+            if (lane == 0) {  // the slots are free again: their reads above come first
+                __threadfence_block();
+                *reinterpret_cast<volatile unsigned long long*>(&s_tree_done) = (unsigned long long)(k + m);
+            }
             lap(kPhTreeWork);
             const bool mine = lane < m;
             const Item it = ph_decode<A>(a, mine ? my_item : 0);
@@ -268,6 +271,23 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
         bool fail = false;
         int h = half;   // half-stage of this warp's next use (u = 2 k + half), incrementally
         uint32_t pu = 0;  // ... and that half-stage's use number u / H
+        // slot ks % T may be rewritten once the tree warp has consumed use ks - T of it: a
+        // monotonic count in shared memory, read only when this warp's last view of it does not
+        // already cover the slot (an mbarrier per slot cost a try_wait per block and warp)
+        unsigned long long done = 0;  // this warp's last view of s_tree_done
+        auto slot_free = [&](long long kq) -> bool {
+            if ((unsigned long long)(kq - T) < done) return true;
+            const unsigned long long t0 = globaltimer_ns();
+            for (unsigned i = 0;; ++i) {
+                done = *reinterpret_cast<volatile unsigned long long*>(&s_tree_done);
+                if ((unsigned long long)(kq - T) < done) return true;
+                __nanosleep(32);  // rare: do not take issue slots from the other compute warps
+                if ((i & 63u) == 63u && (aborted(err) || globaltimer_ns() - t0 > kWaitTimeoutNs)) {
+                    raise_abort(err, 16u);
+                    return false;
+                }
+            }
+        };
         for (;; h += 2) {
             if (h >= H) h -= H, ++pu;
             lap(kPhP2Work);
@@ -286,7 +306,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
                 const bool clamped = warp_pass1<V>(v, valid, &wp);
                 const int t = (int)(ks % T);
                 lap(kPhP1Work);
-                if (ks >= T && !wait_or_abort(&tempty[t], (uint32_t)(((ks / T) - 1) & 1), err, 16u)) { fail = true; break; }
+                if (ks >= T && !slot_free(ks)) { fail = true; break; }
                 lap(kPhP1Slot);
                 if (lane == 0) {
                     wpairs[t][warp] = wp;
@@ -324,7 +344,7 @@ __global__ void __launch_bounds__(kPhThreads, 1) rowph_kernel(const KArgs a) {
         // end mark for the tree warp (its loop stops at the first slot holding -1)
         if (A != kFinish && !fail) {
             const int t = (int)(ks % T);
-            if (!(ks >= T && !wait_or_abort(&tempty[t], (uint32_t)(((ks / T) - 1) & 1), err, 16u))) {
+            if (!(ks >= T && !slot_free(ks))) {
                 if (warp == 0 && lane == 0) slot_item[t] = -1;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tfull[t]);
