@@ -332,6 +332,14 @@ int tp_phase_only(int algo, int in_dtype, int phase, const void* x, float* y, in
 int tp_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, float* sink,
                   cudaStream_t stream);
 
+/* HBM copy-throughput probe (measurement only): y = x over the first floor(bytes / chunk_bytes)
+ * chunks with bulk (TMA) copies both ways, CTA c taking chunks c, c + ctas, ... (descending when
+ * backward != 0) through a ring of `stages` shared-memory buffers; each chunk is stored straight
+ * from its stage.  Limits as tp_read_probe; x, y device, 16-byte aligned, not overlapping.
+ * Asynchronous; TP_EINVAL on bad arguments. */
+int tp_copy_probe(const void* x, void* y, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, int backward,
+                  cudaStream_t stream);
+
 /* Accuracy sweep hook (test/metrology only): for i < count, x = the fp32 whose
  * bit pattern is bits0 + i (the caller keeps bits0 + count - 1 <= 0xffffffff); what = 0:
  * ExtExp -> out0 = m, out1 = n; what = 1: Exp with reconstruction (Alg. 4,

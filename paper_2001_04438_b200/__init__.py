@@ -34,7 +34,7 @@ EXPORTS = [
     "softmax_bf16_partial", "softmax_f32_finish", "softmax_bf16_f32_finish", "softmax_workspace_bytes",
     "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_partial_push_ex", "softmax_finish_mailbox_ex", "softmax_f32_host", "softmax_bf16_f32_host",
     "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
-    "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_read_probe", "tp_phase_only", "tp_exp_sweep", "tp_exp_fit",
+    "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_read_probe", "tp_copy_probe", "tp_phase_only", "tp_exp_sweep", "tp_exp_fit",
     "softmax3_max_partial_ex", "softmax3_sum_partial_ex", "softmax3_finish_ex",
     "tp_mailbox_bytes", "tp_mailbox_pairs_offset", "tp_pairs_push", "tp_pairs_wait", "tp_ipc_get_handle", "tp_ipc_open", "tp_ipc_close",
 ]
@@ -108,6 +108,7 @@ def lib() -> ctypes.CDLL:
         L.tp_exp_sweep.argtypes = [ci, ctypes.c_uint32, i64, vp, vp, vp]
         L.tp_stream_baseline.argtypes = [ci, vp, vp, i64, ctypes.c_float, i64, vp]
         L.tp_read_probe.argtypes = [vp, i64, i64, ci, i64, vp, vp]
+        L.tp_copy_probe.argtypes = [vp, vp, i64, i64, ci, i64, ci, vp]
         L.tp_phase_only.argtypes = [ci, ci, ci, vp, vp, i64, i64, vp, ctypes.c_size_t, vp]
         L.tp_bench_compute.argtypes = [ci, ci, i64, ci, vp, vp]
         L.softmax_last_plan.argtypes = [ctypes.POINTER(SoftmaxPlan)]

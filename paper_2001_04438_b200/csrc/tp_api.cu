@@ -673,6 +673,17 @@ int tp_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages,
     return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 
+int tp_copy_probe(const void* x, void* y, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, int backward,
+                  cudaStream_t stream) {
+    if (!x || !y || bytes < 0 || chunk_bytes < 16 || (chunk_bytes & 15) || stages < 1 || stages > 32 ||
+        chunk_bytes * stages > 227 * 1024 || ctas < 1 || (reinterpret_cast<uintptr_t>(x) & 15) ||
+        (reinterpret_cast<uintptr_t>(y) & 15))
+        return TP_EINVAL;
+    if (bytes < chunk_bytes) return TP_OK;
+    cudaError_t e = tp::launch_copy_probe(x, y, bytes, chunk_bytes, stages, ctas, backward, stream);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
 int tp_exp_sweep(int what, uint32_t bits0, int64_t count, float* out0, float* out1, cudaStream_t stream) {
     if (what < 0 || what > 1 || count < 0 || (count > 0 && (!out0 || (what == 0 && !out1))) ||
         (uint64_t)bits0 + (uint64_t)count > 0x100000000ull)

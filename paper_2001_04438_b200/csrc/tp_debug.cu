@@ -258,6 +258,51 @@ cudaError_t launch_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes,
     return cudaGetLastError();
 }
 
+// Copy probe (measurement only): y = x by bulk (TMA) copies both ways, one thread per CTA: chunk
+// j lands in stage j mod stages, is stored from there with a bulk store, and the stage is reloaded
+// once that store has read it.  backward != 0: a CTA walks its chunks in descending order.
+__global__ void copy_tma_kernel(const char* x, char* y, int64_t nchunks, uint32_t chunk_bytes, int stages,
+                                int backward) {
+    extern __shared__ __align__(128) unsigned char buf[];
+    __shared__ __align__(8) uint64_t bar[32];
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < stages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    const int64_t mine = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto chunk = [&](int64_t j) -> int64_t {  // this CTA's j-th chunk
+        const int64_t q = backward ? mine - 1 - j : j;
+        return blockIdx.x + q * gridDim.x;
+    };
+    const uint64_t keep = policy_evict_first();
+    for (int64_t j = 0; j < stages && j < mine; ++j) {
+        mbar_arrive_expect_tx(&bar[j], chunk_bytes);
+        tma_load_1d(buf + (size_t)j * chunk_bytes, x + chunk(j) * chunk_bytes, chunk_bytes, &bar[j], keep);
+    }
+    unsigned par = 0;
+    for (int64_t j = 0; j < mine; ++j) {
+        const int s = (int)(j % stages);
+        mbar_wait_parity(&bar[s], (par >> s) & 1u);
+        par ^= 1u << s;
+        tma_store_1d(y + chunk(j) * chunk_bytes, buf + (size_t)s * chunk_bytes, chunk_bytes, keep);
+        bulk_commit();
+        if (j + stages < mine) {
+            bulk_wait_read<0>();  // this stage's store has read shared memory
+            mbar_arrive_expect_tx(&bar[s], chunk_bytes);
+            tma_load_1d(buf + (size_t)s * chunk_bytes, x + chunk(j + stages) * chunk_bytes, chunk_bytes, &bar[s], keep);
+        }
+    }
+    bulk_wait<0>();
+}
+
+cudaError_t launch_copy_probe(const void* x, void* y, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas,
+                              int backward, cudaStream_t s) {
+    const size_t dyn = (size_t)chunk_bytes * stages;
+    cudaFuncSetAttribute(copy_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    copy_tma_kernel<<<(unsigned)ctas, 32, dyn, s>>>(static_cast<const char*>(x), static_cast<char*>(y),
+                                                   bytes / chunk_bytes, (uint32_t)chunk_bytes, stages, backward);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_stream_baseline(int what, float* x, float* y, int64_t n, float a, int64_t ctas, cudaStream_t s) {
     if (what == 4) read_deep_kernel<8><<<(unsigned)ctas, 512, 0, s>>>(x, y, n / 4);
     else if (what == 5) read_deep_kernel<16><<<(unsigned)ctas, 512, 0, s>>>(x, y, n / 4);

@@ -133,6 +133,8 @@ struct Shard3 {
 };
 cudaError_t launch_shard3(int algo, int in_bf16, int phase, const void* x, float* y, int64_t rows, int64_t cols,
                           void* ws, const Shard3& sh, const LaunchOpts& o, cudaStream_t s);
+cudaError_t launch_copy_probe(const void* x, void* y, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas,
+                              int backward, cudaStream_t s);
 cudaError_t launch_read_probe(const void* x, int64_t bytes, int64_t chunk_bytes, int stages, int64_t ctas, float* y,
                               cudaStream_t s);
 cudaError_t launch_exp_sweep(int what, uint32_t bits0, int64_t count, float* o0, float* o1, cudaStream_t s);
