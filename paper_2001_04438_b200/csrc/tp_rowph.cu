@@ -48,11 +48,11 @@ constexpr int64_t kPhMaxRows = 8;          // Two-Pass: rows of one launch (pass
 #endif
 constexpr unsigned long long kPhChunk = TP_PH_CHUNK;  // items per queue claim
 
-// Staging: H half-block stages, H even, so that half-stage h always holds the same half of its
-// blocks (h even: first halves, read by warps 0-7; h odd: second halves, warps 8-15) and each
-// half frees as soon as its own 8 warps have read it: 6 x 32 KB fp32 / 12 x 16 KB bf16 = 192 KB.
-// (An odd H, 7 x 32 KB, would hold more bytes in flight, but then one half-stage serves both
-// halves in turn and the halves must stay in lockstep: measured 20% slower.)
+// Staging: H half-block stages; a half frees as soon as its own 8 warps (0-7: first halves,
+// 8-15: second halves) have read it: 6 x 32 KB fp32 / 12 x 16 KB bf16 = 192 KB.  With H even a
+// half-stage always holds the same half; an odd H (7 x 32 KB = 224 KB, TP_PH_H32=7) is correct
+// too (full barriers per half, below) but measured no faster: more staging does not help pass 1,
+// whose gap to the read ceiling is its arithmetic.
 #ifndef TP_PH_H32
 #define TP_PH_H32 6
 #endif
