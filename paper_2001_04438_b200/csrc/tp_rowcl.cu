@@ -72,6 +72,15 @@ enum ClProf : int {
     kProfFreeStageWait, kProfPushWait, kProfProducerTotal, kProfCtas, kProfTeamBTotal
 };
 
+// development timeline (PROF launches, tools/prof_cl_timeline.py): globaltimer stamps per CTA and
+// row iteration k < kClTlRows at prof[16 + (cta * kClTlRows + k) * 8 + slot]
+constexpr int kClTlRows = 16;
+enum ClTl : int { kTlLoadA = 0, kTlA0, kTlA1, kTlTree, kTlStats, kTlB0, kTlBStats, kTlB1 };
+template <bool PROF>
+__device__ __forceinline__ void cl_stamp(const KArgs& a, int k, int slot) {
+    if (PROF && k < kClTlRows) a.prof[16 + ((size_t)blockIdx.x * kClTlRows + k) * 8 + slot] = globaltimer_ns();
+}
+
 struct ClCmd {
     int op;
     int stage;        // the block's half-stages and full-barrier parities: s0 | p0 << 4 | s1 << 5 | p1 << 9
@@ -235,30 +244,22 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             mbar_arrive(&cfull_bar[team][c]);
             ++pushed;
         };
-        // a free half-stage of this pool (its previous use fully read), round robin
+        // the next half-stage of this pool, in ring order, once its previous use is fully read.
+        // A team reads its commands in order and every warp releases a block's half 0 before
+        // its half 1, so half-stages free in the order they were filled: waiting on the next
+        // one in the ring (try_wait: the thread sleeps until the barrier completes) never waits
+        // longer than needed.  (Round 1 scanned the pool with test_wait, ~150 cycles per busy
+        // stage per pass: a freed stage was seen up to ~900 cycles late; C4 bf16 333 -> 323 us.)
         auto free_stage = [&]() -> int {
-            const unsigned long long t0 = globaltimer_ns();
-            const unsigned long long c0 = PROF ? clock64() : 0ull;
-            for (unsigned i = 0;; ++i) {
-                for (int j = 0; j < s_hi - s_lo; ++j) {
-                    int s = rr + j;
-                    s = s >= s_hi ? s - (s_hi - s_lo) : s;
-                    if (((busy >> s) & 1u) && mbar_test_parity(&empty_bar[s], ((use_par >> s) & 1u) ^ 1u))
-                        busy &= ~(1u << s);
-                    if (!((busy >> s) & 1u)) {
-                        rr = s + 1 == s_hi ? s_lo : s + 1;
-                        if (PROF) pc_free += clock64() - c0;
-                        return s;
-                    }
-                }
-                if ((i & 63u) == 63u) {
-                    if (aborted(err)) return -1;
-                    if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
-                        raise_abort(err, 128u);
-                        return -1;
-                    }
-                }
+            const int s = rr;
+            rr = s + 1 == s_hi ? s_lo : s + 1;
+            if ((busy >> s) & 1u) {
+                const unsigned long long c0 = PROF ? clock64() : 0ull;
+                if (!wait_or_abort(&empty_bar[s], ((use_par >> s) & 1u) ^ 1u, err, 128u)) return -1;
+                if (PROF) pc_free += clock64() - c0;
+                busy &= ~(1u << s);
             }
+            return s;
         };
         // L2 policy per load kind (KArgs::l2_hints, env TP_L2_HINTS): 1 keep = evict_last for the
         // pass-1 loads pass 2 re-reads, drop = evict_first for the re-reads (default); 0 none;
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                         break;
                     }
                 }
+                cl_stamp<PROF>(a, k, kTlLoadA);
                 for (int li = 0; li < nloc && ok; ++li) {
                     const int st = load(row, b_lo + li, true);
                     if (st < 0) { ok = false; break; }
@@ -383,6 +385,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 }
             }
             if (!ok) break;
+            if (lane == 0) cl_stamp<PROF>(a, k, kTlTree);
             // the local blocks' clamp masks for team B's pass 2, in the workspace by (row, block):
             // a shared slot per row parity could be rewritten two rows later while team B still
             // reads it (team B can trail the tree warp by more than a row when shares are short)
@@ -401,6 +404,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             if (lane == 0) {
                 if (anyc) __threadfence_block();  // the block_clamp stores (all lanes) before the flag
                 row_st[k % kClStSlots] = make_float4(st.x, st.y, anyc ? 1.0f : 0.0f, 0.0f);
+                cl_stamp<PROF>(a, k, kTlStats);
                 mbar_arrive(&st_bar[k % kClStSlots]);
             }
         }
@@ -417,6 +421,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     const int pw = teamB ? warp - kClTeam : warp;
     float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
     long long np1 = 0;  // pass-1 blocks handed to the tree warp (team A)
+    int tl_k = -1;      // development timeline: row iteration of team A's last command
     unsigned long long pc[kProfComputeTotal] = {0, 0, 0, 0, 0};
     const unsigned long long pc_start = PROF ? clock64() : 0ull;
     unsigned long long tq = pc_start;
@@ -443,7 +448,12 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
         const int st_pack = cmd.stage;
         BlockVals v;
         bool fail = false;
+        const bool tl = PROF && pw == 0 && lane == 0;
         if (!teamB) {
+            if (tl && cmd.k != tl_k) {
+                cl_stamp<PROF>(a, cmd.k, kTlA0);
+                tl_k = cmd.k;
+            }
             const int sl = (int)(np1 % T);
             if (np1 >= T && !wait_or_abort(&tp_empty[sl], (uint32_t)(((np1 / T) - 1) & 1), err, 1024u)) break;
             ++np1;
@@ -467,12 +477,15 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
             if (fail) break;
             __syncwarp();
             if (lane == 0) mbar_arrive(&tp_full[sl]);
+            if (tl) cl_stamp<PROF>(a, cmd.k, kTlA1);
         } else {
             if (cmd.flags & kClFirstP2) {  // the row's statistics, from the tree warp
+                if (tl) cl_stamp<PROF>(a, cmd.k, kTlB0);
                 const int ss = cmd.k % kClStSlots;
                 if (!wait_or_abort(&st_bar[ss], (uint32_t)((cmd.k / kClStSlots) & 1), err, 256u)) break;
                 st = row_st[ss];
                 lap(kProfRowWait);
+                if (tl) cl_stamp<PROF>(a, cmd.k, kTlBStats);
             }
             const unsigned mask = st.z != 0.0f   // some local block of the row took the clamped path
                 ? __ldcg(reinterpret_cast<const unsigned*>(a.ws + a.lay.block_clamp) + row * a.nb + blk) : 0u;
@@ -491,6 +504,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
                 lap(kProfP2);
             }
             if (fail) break;
+            if (tl) cl_stamp<PROF>(a, cmd.k, kTlB1);
         }
     }
     if (PROF && pw == 0 && lane == 0) {
