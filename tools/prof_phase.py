@@ -14,7 +14,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-_PROF_SO = os.path.join(ROOT, "paper_2001_04438_b200", "libtwopass_prof.so")
+_PROF_SO = os.environ.get("TP_PROF_LIBRARY") or os.path.join(ROOT, "paper_2001_04438_b200", "libtwopass_prof.so")
 os.environ["TP_LIBRARY"] = _PROF_SO  # before the package import: the binding reads it then
 from paper_2001_04438_b200 import build as _build  # noqa: E402
 if not os.path.exists(_PROF_SO):
