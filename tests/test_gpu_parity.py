@@ -578,6 +578,24 @@ def test_three_pass_cluster_schedule_agrees_bitwise(rows, cols, dtype):
             assert_parity(x, ref, f"{algo} cluster")
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_three_pass_cluster_many_rows_per_cluster(dtype):
+    # a few clusters, many rows each: the bf16 kernel's software pipeline over a CTA's rows runs
+    # through its four exchange buffers many times (tp_rowcl3.cu rowcl3p_kernel); fp32 the
+    # sequential kernel.  Bitwise the stream kernel.
+    x = workloads.ragged_case(64, 16384 * 6 + 100, -300, 300, seed=21, stream=7)
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    for algo in ("recompute", "reload"):
+        ref = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_STREAM))
+        for cl, g in ((2, 4), (4, 4), (1, 3)):
+            y = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_CLUSTER, cluster_size=cl, grid_ctas=g))
+            assert np.array_equal(ref, y), (algo, cl, g, tp.last_plan())
+        assert tp.watchdog_flags() == 0
+        assert_parity(x, ref, f"{algo} many rows per cluster")
+
+
 @pytest.mark.parametrize("cl", [1, 2])
 def test_cluster_clamp_masks_with_short_shares(cl):
     # regression (found by tools/soak.py): with short shares team B of the cluster kernel could
