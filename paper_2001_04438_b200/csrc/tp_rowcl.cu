@@ -78,7 +78,8 @@ enum ClFlag : int { kClFirstP2 = 2 };
 // development counters (KArgs::prof): clock cycles summed over CTAs
 enum ClProf : int {
     kProfCmdWait = 0, kProfFullWait, kProfRowWait, kProfP1, kProfP2, kProfComputeTotal,
-    kProfFreeStageWait, kProfPushWait, kProfProducerTotal, kProfCtas, kProfTeamBTotal
+    kProfFreeStageWait, kProfPushWait, kProfProducerTotal, kProfCtas, kProfTeamBTotal,
+    kProfFullWaitB, kProfCmdWaitB  // team B's share of kProfFullWait / kProfCmdWait
 };
 
 // development timeline (PROF launches, tools/prof_cl_timeline.py): globaltimer stamps per CTA and
@@ -521,6 +522,10 @@ __global__ void __launch_bounds__(kClThreads, 1) rowcl_kernel(const KArgs a, int
     }
     if (PROF && pw == 0 && lane == 0) {
         for (int i = 0; i < kProfComputeTotal; ++i) atomicAdd(&a.prof[i], pc[i]);
+        if (teamB) {
+            atomicAdd(&a.prof[kProfFullWaitB], pc[kProfFullWait]);
+            atomicAdd(&a.prof[kProfCmdWaitB], pc[kProfCmdWait]);
+        }
         atomicAdd(&a.prof[teamB ? kProfTeamBTotal : kProfComputeTotal], clock64() - pc_start);
     }
 }

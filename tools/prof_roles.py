@@ -18,7 +18,8 @@ import paper_2001_04438_b200 as tp  # noqa: E402
 import workloads  # noqa: E402
 
 SLOTS = ["cmd_wait", "full_wait", "row_wait_and_stats", "p1_compute", "p2_compute", "teamA_total",
-         "prod_free_stage_wait", "prod_push_wait", "prod_total", "ctas", "teamB_total"]
+         "prod_free_stage_wait", "prod_push_wait", "prod_total", "ctas", "teamB_total", "teamB_full_wait",
+         "teamB_cmd_wait"]
 
 
 def main():
@@ -43,7 +44,7 @@ def main():
     tp.lib().tp_set_profile_buffer(None)
     c = buf.cpu().numpy().astype(np.float64)
     ctas = c[9]
-    per = {SLOTS[i]: c[i] / ctas for i in range(11) if i != 9}
+    per = {SLOTS[i]: c[i] / ctas for i in range(13) if i != 9}
     tot = per["teamA_total"] + per["teamB_total"]
     out = {"config": args.config, "plan": tp.last_plan(), "us_per_launch": s.elapsed_time(e) * 1e3 / args.reps,
            "cycles_per_cta": {k: round(v) for k, v in per.items()},
