@@ -246,6 +246,21 @@ int softmax_finish_mailbox_ex(int in_dtype, const void* x, float* y, int64_t row
 int softmax_f32_host(const float* hx, float* hy, int64_t rows, int64_t cols);
 int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t cols);
 
+/* Asynchronous form of the host-buffer call (throughput: consecutive calls overlap, one call's
+ * host->device copies with the previous call's device->host copies, the two PCIe directions at
+ * once).  Enqueues the copies and kernels of one call on the library's internal streams of the
+ * current device and returns; *ticket identifies the call.  Submitted calls alternate between two
+ * internal staging slots (device memory for x and y of one call each, cached), so at most two run
+ * at a time; a third submission queues behind the first on its slot.
+ * in_dtype: TP_IN_F32 / TP_IN_BF16.  hx, hy: HOST pointers (pinned for full bandwidth) that must
+ * stay valid and untouched until softmax_host_wait(ticket) returns.  Results are bit-identical to
+ * softmax_f32_host.  Returns TP_EINVAL for bad arguments or a NULL ticket pointer.              */
+int softmax_host_submit(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t cols,
+                        unsigned long long* ticket);
+/* Blocks until the call `ticket` (and every earlier call on its slot) has completed and hy is
+ * filled.  A ticket more than 15 submissions old on its device is rejected (TP_EINVAL).       */
+int softmax_host_wait(unsigned long long ticket);
+
 /* ---- status ---------------------------------------------------------------- */
 /* What the last launch issued by this host thread ran (diagnostics; no device work):
  * kernel = 1 general (any alignment), 2 stream (persistent grid), 3 cluster (one

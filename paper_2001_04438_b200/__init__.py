@@ -32,7 +32,7 @@ EXPORTS = [
     "softmax_f32", "softmax_bf16_f32", "softmax3_recompute_f32", "softmax3_reload_f32",
     "softmax3_recompute_bf16_f32", "softmax3_reload_bf16_f32", "softmax_f32_partial",
     "softmax_bf16_partial", "softmax_f32_finish", "softmax_bf16_f32_finish", "softmax_workspace_bytes",
-    "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_partial_push_ex", "softmax_finish_mailbox_ex", "softmax_f32_host", "softmax_bf16_f32_host",
+    "softmax_ex", "softmax_partial_ex", "softmax_finish_ex", "softmax_partial_push_ex", "softmax_finish_mailbox_ex", "softmax_f32_host", "softmax_bf16_f32_host", "softmax_host_submit", "softmax_host_wait",
     "softmax_status_str", "softmax_last_cuda_error", "softmax_watchdog_flags", "softmax_last_plan", "tp_debug_op",
     "tp_bench_compute", "tp_set_profile_buffer", "tp_stream_baseline", "tp_read_probe", "tp_copy_probe", "tp_phase_only", "tp_exp_sweep", "tp_exp_fit",
     "softmax3_max_partial_ex", "softmax3_sum_partial_ex", "softmax3_finish_ex",
@@ -90,6 +90,8 @@ def lib() -> ctypes.CDLL:
         L.softmax3_finish_ex.argtypes = [ci, ci, vp, vp, i64, i64, vp, vp, ci, vp, sz, vp]
         L.softmax_f32_host.argtypes = [vp, vp, i64, i64]
         L.softmax_bf16_f32_host.argtypes = [vp, vp, i64, i64]
+        L.softmax_host_submit.argtypes = [ctypes.c_int, vp, vp, i64, i64, ctypes.POINTER(ctypes.c_ulonglong)]
+        L.softmax_host_wait.argtypes = [ctypes.c_ulonglong]
         L.softmax_status_str.argtypes = [ci]
         L.softmax_status_str.restype = ctypes.c_char_p
         L.tp_debug_op.argtypes = [ci, vp, vp, vp, vp, i64, vp]
@@ -336,6 +338,23 @@ def softmax_host(hx: torch.Tensor, hy: torch.Tensor | None = None) -> torch.Tens
     f = lib().softmax_f32_host if _in_dtype(hx) == IN_F32 else lib().softmax_bf16_f32_host
     _check(f(hx.data_ptr(), hy.data_ptr(), rows, cols), "softmax_host")
     return hy
+
+
+def softmax_host_submit(hx: torch.Tensor, hy: torch.Tensor) -> int:
+    """Asynchronous end-to-end softmax of a HOST tensor into a host fp32 tensor: returns a ticket
+    for host_wait(); consecutive submissions overlap (include/twopass.h softmax_host_submit).
+    hx and hy must stay alive and untouched until host_wait(ticket) returns."""
+    assert not hx.is_cuda and hx.is_contiguous()
+    assert not hy.is_cuda and hy.is_contiguous() and hy.dtype == torch.float32 and hy.shape == hx.shape
+    rows, cols = _rows_cols(hx)
+    t = ctypes.c_ulonglong(0)
+    _check(lib().softmax_host_submit(_in_dtype(hx), hx.data_ptr(), hy.data_ptr(), rows, cols, ctypes.byref(t)),
+           "softmax_host_submit")
+    return t.value
+
+
+def host_wait(ticket: int) -> None:
+    _check(lib().softmax_host_wait(ticket), "softmax_host_wait")
 
 
 def last_plan() -> dict:

@@ -28,11 +28,9 @@ constexpr size_t kHostSlabBytes = 64ull << 20;  // host pipeline: input bytes pe
 // Measured on B200 (tools/pcie_probe.py, C4): H2D 14.8 ms and D2H 15.2 ms alone, 17.0 ms at
 // once; 2 streams x 64 MB slabs 18.1 ms end to end; smaller slabs or more streams are slower.
 
-struct DevState {
-    std::mutex mu;
-    void* ws = nullptr;
-    size_t ws_bytes = 0;
-    // host pipeline, row slabs: one staging slot per stream
+// One in-flight host-buffer call: its streams, events and device staging (cached between calls).
+struct HostSlot {
+    // row slabs: one staging slot per stream
     void* hx_dev[kHostStreams] = {};
     float* hy_dev[kHostStreams] = {};
     size_t stage_bytes_x = 0, stage_bytes_y = 0;
@@ -49,6 +47,19 @@ struct DevState {
     cudaStream_t st[kHostStreams] = {};
     cudaEvent_t ev[64];
     bool ev_init = false;
+};
+// slot 0: the synchronous call; 1 and 2: submitted calls in turn, so that one call's uploads
+// overlap the previous call's downloads (the two PCIe directions at once)
+constexpr int kHostSlots = 3;
+constexpr int kTicketEvents = 16;  // submitted calls that can be waited for individually
+struct DevState {
+    std::mutex mu;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    HostSlot hs[kHostSlots];
+    unsigned long long tickets = 0;
+    cudaEvent_t tev[kTicketEvents];
+    bool tev_init = false;
 };
 DevState g_dev[kMaxDev];
 
@@ -246,14 +257,11 @@ int run_finish(int in_dtype, const void* x, float* y, int64_t rows, int64_t cols
 }
 
 // ---------------------------------------------------------------- host-buffer pipeline
-int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t cols) {
-    int st = check_args(in_dtype, hx, hy, rows, cols, true);
-    if (st) return st;
-    int dev;
-    st = current_device(&dev);
-    if (st) return st;
-    DevState& d = g_dev[dev];
-    std::lock_guard<std::mutex> lk(d.mu);
+// Enqueue one call on the slot's streams (caller holds the device lock); *last = the stream
+// whose completion completes the call.
+int host_enqueue(HostSlot& d, int in_dtype, const void* hx, float* hy, int64_t rows, int64_t cols,
+                 cudaStream_t* last) {
+    int st = TP_OK;
     cudaError_t e;
     if (!d.st[0]) {
         for (int i = 0; i < kHostStreams; ++i) {
@@ -312,8 +320,8 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
             e = cudaMemcpyAsync(hy + (size_t)c * cl, dy + (size_t)c * cl, (size_t)cl * 4, cudaMemcpyDeviceToHost, cp);
             if (e != cudaSuccess) return cuda_fail(e);
         }
-        e = cudaStreamSynchronize(cp);
-        return e == cudaSuccess ? TP_OK : cuda_fail(e);
+        *last = cp;
+        return TP_OK;
     }
 
     // Row slabs of ~64 MB round-robin over 2 streams: the H2D copy of the next slab, the kernel
@@ -403,11 +411,66 @@ int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t
         e = cudaMemcpyAsync(hy + (size_t)(r0 * cols), d.hy_dev[k], (size_t)(nr * cols) * 4, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_fail(e);
     }
-    for (int i = 0; i < kHostStreams; ++i) {
-        e = cudaStreamSynchronize(d.st[i]);
-        if (e != cudaSuccess) return cuda_fail(e);
+    for (int i = 1; i < kHostStreams; ++i) {  // the call ends on stream 0
+        cudaEventRecord(d.ev[i], d.st[i]);
+        cudaStreamWaitEvent(d.st[0], d.ev[i], 0);
     }
+    *last = d.st[0];
     return TP_OK;
+}
+
+int host_pipeline(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t cols) {
+    int st = check_args(in_dtype, hx, hy, rows, cols, true);
+    if (st) return st;
+    int dev;
+    st = current_device(&dev);
+    if (st) return st;
+    DevState& d = g_dev[dev];
+    std::lock_guard<std::mutex> lk(d.mu);
+    cudaStream_t last = nullptr;
+    if ((st = host_enqueue(d.hs[0], in_dtype, hx, hy, rows, cols, &last))) return st;
+    const cudaError_t e = cudaStreamSynchronize(last);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
+}
+
+int host_submit(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t cols, unsigned long long* ticket) {
+    int st = check_args(in_dtype, hx, hy, rows, cols, true);
+    if (st) return st;
+    if (!ticket) return TP_EINVAL;
+    int dev;
+    st = current_device(&dev);
+    if (st) return st;
+    DevState& d = g_dev[dev];
+    std::lock_guard<std::mutex> lk(d.mu);
+    if (!d.tev_init) {
+        for (auto& ev : d.tev) {
+            const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+        d.tev_init = true;
+    }
+    const unsigned long long t = ++d.tickets;
+    cudaStream_t last = nullptr;
+    if ((st = host_enqueue(d.hs[1 + (t & 1)], in_dtype, hx, hy, rows, cols, &last))) return st;
+    const cudaError_t e = cudaEventRecord(d.tev[t % kTicketEvents], last);
+    if (e != cudaSuccess) return cuda_fail(e);
+    *ticket = (unsigned long long)dev << 48 | t;
+    return TP_OK;
+}
+
+int host_wait(unsigned long long ticket) {
+    const int dev = (int)(ticket >> 48);
+    const unsigned long long t = ticket & ((1ull << 48) - 1);
+    if (dev < 0 || dev >= kMaxDev || t == 0) return TP_EINVAL;
+    DevState& d = g_dev[dev];
+    cudaEvent_t ev;
+    {
+        std::lock_guard<std::mutex> lk(d.mu);
+        if (!d.tev_init || t > d.tickets || d.tickets - t >= (unsigned long long)kTicketEvents) return TP_EINVAL;
+        ev = d.tev[t % kTicketEvents];
+    }
+    const cudaError_t e = cudaEventSynchronize(ev);
+    return e == cudaSuccess ? TP_OK : cuda_fail(e);
 }
 
 }  // namespace
@@ -567,6 +630,11 @@ int softmax_f32_host(const float* hx, float* hy, int64_t rows, int64_t cols) {
 int softmax_bf16_f32_host(const uint16_t* hx, float* hy, int64_t rows, int64_t cols) {
     return host_pipeline(TP_IN_BF16, hx, hy, rows, cols);
 }
+int softmax_host_submit(int in_dtype, const void* hx, float* hy, int64_t rows, int64_t cols,
+                        unsigned long long* ticket) {
+    return host_submit(in_dtype, hx, hy, rows, cols, ticket);
+}
+int softmax_host_wait(unsigned long long ticket) { return host_wait(ticket); }
 const char* softmax_status_str(int status) {
     switch (status) {
         case TP_OK: return "ok";

@@ -410,6 +410,28 @@ def test_host_pipeline_slab_ramp_bitwise():
     assert np.array_equal(hy.numpy(), to_host(tp.softmax(to_dev(x))))
 
 
+def test_host_submit_overlapping_calls_bitwise():
+    # the asynchronous host-buffer call: calls in flight on the two staging slots (and a third
+    # queued behind the first), each result the synchronous call's bits; single long row (chunked
+    # path) and row slabs (bf16 and fp32)
+    cases = [workloads.generate("c3")[:, : 1 << 24], workloads.generate("c4", 0, 40)]
+    xb = workloads.generate("c4b", 0, 30)
+    hxs = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in cases]
+    hxs.append(torch.from_numpy(xb.view(np.int16)).view(torch.bfloat16).pin_memory())
+    for hx in hxs:
+        ref = tp.softmax_host(hx)
+        hys = [torch.empty(hx.shape, dtype=torch.float32).pin_memory() for _ in range(3)]
+        tickets = [tp.softmax_host_submit(hx, hy) for hy in hys]
+        for t in reversed(tickets):
+            tp.host_wait(t)
+        for hy in hys:
+            assert torch.equal(hy, ref)
+    with pytest.raises(tp.TwoPassError):
+        tp.host_wait(0)
+    with pytest.raises(tp.TwoPassError):
+        tp.host_wait(tickets[-1] + 1)  # not submitted yet
+
+
 def test_host_pipeline_bf16_and_multi_slab():
     x = workloads.generate("c4b", 0, 40)
     hx = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
