@@ -227,7 +227,7 @@ def cpu_baseline(args, spec):
 
 KERNEL_NAMES = {"stream": "tp::stream_kernel<{In},kTwoPass>", "cluster": "tp::rowcl_kernel<{In}>",
                 "general": "tp::general_kernel<{In},kTwoPass>", "small": "tp::small_kernel<{In}>",
-                "phase": "tp::rowph_kernel<{In},kTwoPass>"}
+                "phase": "tp::rowph_kernel<{In},kTwoPass>", "resident": "tp::rowres_kernel<{In}>"}
 
 
 def traffic_from_profiles(workload: str, kernel: str):

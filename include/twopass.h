@@ -185,6 +185,12 @@ int tp_ipc_close(void* dev_ptr);
                              any): one CTA per SM taking all pass-1 blocks, then all pass-2
                              blocks, from an in-order queue, no command ring (AUTO picks it for
                              the Two-Pass from ~100 blocks per SM, the partial from ~48) */
+#define TP_SCHED_RESIDENT 6  /* Two-Pass rows of 4..64 blocks whose share fits shared memory
+                                (bf16: <= 7 blocks per CTA, fp32: <= 3): a group of CTAs per
+                                row stages its whole share, exchanges block values through the
+                                workspace, and runs pass 2 on the staged blocks (the row is read
+                                from HBM once); cluster_size = CTAs per row (0 = automatic;
+                                AUTO picks it for bf16 rows of 4..64 blocks, one block per CTA) */
 typedef struct {
     int64_t grid_ctas;
     int64_t lookahead_rows;

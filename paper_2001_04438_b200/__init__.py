@@ -25,7 +25,7 @@ _SO = os.environ.get("TP_LIBRARY") or os.path.join(_PKG, "libtwopass.so")
 
 TP_OK, TP_EINVAL, TP_ECUDA, TP_ENODEV, TP_EWATCHDOG = 0, 1, 2, 3, 4
 ALGO_TWO_PASS, ALGO_RECOMPUTE, ALGO_RELOAD = 0, 2, 3
-SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER, SCHED_SMALL, SCHED_PHASE = 0, 1, 2, 3, 4, 5  # TP_SCHED_*
+SCHED_AUTO, SCHED_STREAM, SCHED_HOLD, SCHED_CLUSTER, SCHED_SMALL, SCHED_PHASE, SCHED_RESIDENT = 0, 1, 2, 3, 4, 5, 6  # TP_SCHED_*
 IN_F32, IN_BF16 = 0, 1
 
 EXPORTS = [
@@ -55,7 +55,7 @@ class SoftmaxPlan(ctypes.Structure):
                 ("cluster_size", ctypes.c_int), ("lookahead_rows", ctypes.c_int64), ("hold", ctypes.c_int)]
 
 
-KERNEL_NAMES = {0: "none", 1: "general", 2: "stream", 3: "cluster", 4: "small", 5: "phase"}
+KERNEL_NAMES = {0: "none", 1: "general", 2: "stream", 3: "cluster", 4: "small", 5: "phase", 6: "resident"}
 
 _lib = None
 

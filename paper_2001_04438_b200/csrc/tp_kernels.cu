@@ -272,6 +272,14 @@ static cudaError_t launch_split(const KArgs& a, int CL, int64_t tail, int tail_c
     return launch_stream<In, kTwoPass>(t, oq, s);
 }
 
+// The resident-row schedule is AUTO's choice where it applies (development override
+// TP_RESIDENT=0 for A/B runs against the cluster kernel).
+template <typename In>
+static bool rowres_auto() {
+    static const int on = dev_env_int("TP_RESIDENT", 1);
+    return on != 0;
+}
+
 template <typename In, int A>
 static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t cols, void* ws, float2* pair_out,
                                const float2* pairs_in, int world, const LaunchOpts& o, cudaStream_t s,
@@ -308,6 +316,18 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
         if ((A == kTwoPass || A == kFused || A == kRecompute || A == kReload) && !o.force_persistent &&
             ((o.schedule == 0 && small_applies(a.rows, a.nb, a.vec)) || (o.schedule == 4 && a.nb <= 3)))
             return launch_small<In, (A == kFused ? kTwoPass : A)>(a, o, s);
+        // Two-Pass rows whose share fits shared memory: a group of CTAs per row, the row read
+        // once (tp_rowres.cu)
+        if (A == kTwoPass && (o.schedule == 6 || (o.schedule == 0 && rowres_auto<In>()))) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            const int G = rowres_choose<In>(a.rows, a.nb, device_sms(dev), o.cluster_size);
+            if (G) {
+                const cudaError_t e = launch_rowres<In>(a, G, o, s);
+                if (e != cudaErrorNotSupported) return e;
+                cudaGetLastError();
+            }
+        }
         // Two-Pass rows of a few blocks: one cluster per row, pass 2 from shared memory / L2
         if (A == kTwoPass && (o.schedule == 0 || o.schedule == 3)) {
             int64_t tail = 0;

@@ -283,6 +283,22 @@ __device__ __forceinline__ bool item_needs_stats(const Item& it) {
     return (AlgoTraits<A>::P > 1 && it.phase > 0) || A == kFinish;
 }
 
+// warp_reduce_leaves(kRedPair, n, leaf) for n <= 64, registers only, result in every lane:
+// lane l reduces leaves [l c, l c + c) (c = 2 when next_pow2(n) = 64, else 1), then the warp tree.
+template <typename LeafFn>
+__device__ __forceinline__ Pair warp_tree64(int n, LeafFn leaf) {
+    const int lane = threadIdx.x & 31;
+    Pair v = pair_identity();
+    if (n > 32) {
+        const int b = 2 * lane;
+        if (b < n) v = pair_merge(leaf(b), b + 1 < n ? leaf(b + 1) : pair_identity());
+    } else if (lane < n) {
+        v = leaf(lane);
+    }
+    v = warp_tree_pairs(v);
+    return Pair{__shfl_sync(0xffffffffu, v.m, 0), __shfl_sync(0xffffffffu, v.n, 0)};
+}
+
 // host side (tp_kernels.cu / tp_stream.cu)
 int device_sms(int dev);
 int64_t lookahead_rows(const KArgs& a, int64_t grid, int items_per_cta, const LaunchOpts& o);
@@ -301,5 +317,9 @@ cudaError_t launch_rowcl3(KArgs a, int CL, const LaunchOpts& o, cudaStream_t s);
 bool rowph_applies(int A, int64_t rows, int64_t nb, int sms);
 template <typename In, int A>
 cudaError_t launch_rowph(KArgs a, const LaunchOpts& o, cudaStream_t s);
+template <typename In>
+int rowres_choose(int64_t rows, int64_t nb, int sms, int force_g);
+template <typename In>
+cudaError_t launch_rowres(KArgs a, int G, const LaunchOpts& o, cudaStream_t s);
 
 }  // namespace tp

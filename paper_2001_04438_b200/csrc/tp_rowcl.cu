@@ -123,22 +123,6 @@ __device__ __forceinline__ void cl_share(int nb, int CL, int r, int* b_lo, int* 
     *nloc = ((r + 1) * nb) / CL - *b_lo;
 }
 
-// warp_reduce_leaves(kRedPair, n, leaf) for n <= 64, registers only, result in every lane:
-// lane l reduces leaves [l c, l c + c) (c = 2 when next_pow2(n) = 64, else 1), then the warp tree.
-template <typename LeafFn>
-__device__ __forceinline__ Pair warp_tree64(int n, LeafFn leaf) {
-    const int lane = threadIdx.x & 31;
-    Pair v = pair_identity();
-    if (n > 32) {
-        const int b = 2 * lane;
-        if (b < n) v = pair_merge(leaf(b), b + 1 < n ? leaf(b + 1) : pair_identity());
-    } else if (lane < n) {
-        v = leaf(lane);
-    }
-    v = warp_tree_pairs(v);
-    return Pair{__shfl_sync(0xffffffffu, v.m, 0), __shfl_sync(0xffffffffu, v.n, 0)};
-}
-
 // Row statistics from the row's nb block values: the canonical group trees, then the tree over
 // the groups (tp_ops.cuh retire_batch, reading G8), then (n_sum - 1, 0.5 / m_sum) (readings G9,
 // G10).  Every lane gets the result.

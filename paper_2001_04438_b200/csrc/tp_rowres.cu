@@ -1,0 +1,305 @@
+// Resident-row kernel: Two-Pass softmax (Alg. 3) for rows of 4..64 blocks split
+// over a group of G CTAs whose shares of two consecutive rows fit shared memory (bf16: up to 3
+// blocks per CTA and row, fp32: 1), e.g. config 4 (256 x 800,000 = 49 blocks per row).
+//
+// Why: the cluster kernel (tp_rowcl.cu) runs pass 1 of row k and pass 2 of row k-1 on the same
+// SM at once with two teams of 8 warps; measured, the two passes then share the SM at ~1.65 us per
+// block-pass against ~1.0 us for 16 warps on one pass alone, and pass 2's re-reads miss L2 (bf16:
+// about half of them; a row period is a whole L2 footprint).  Here every CTA stages its share of
+// a row once and keeps it until pass 2: the row is read from HBM once, and all 16 warps run one
+// pass at a time (pass 1 of row k+1, then pass 2 of row k).  A group is any G CTAs of the grid,
+// not one GPC (8-CTA clusters fit only 15 x 8 SMs): its CTAs exchange block values through the
+// workspace.  A first version with one staged row per CTA and CTA barriers around the exchange
+// measured 392 us on C4 bf16 (cluster kernel 350 us on the same box): every group ran pass 1,
+// the exchange and pass 2 in lockstep, so DRAM idled during pass 1 and was oversubscribed by
+// pass 2's stores; with two rows staged the exchange hides behind the next row's pass 1 and
+// the passes alternate at block granularity.
+//
+// Bit-identical to the other kernels: the same per-warp pass 1 (warp_pass1, clamp decision per
+// warp), block tree over the 16 warp values, canonical tree over the row's blocks (one group of
+// nb <= 64 leaves, warp_tree64 as tp_rowcl.cu's cl_row_stats) and pass 2 (op_pass2).
+//
+// Group exchange (global memory, workspace): each block value is stored into the row's
+// block_vals and released by the row ticket (red.release, one per block); a CTA's statistics warp
+// polls the ticket until it reaches nb (acquire), forms the row statistics from the nb values.
+// Tickets only count up during a launch; the last CTA to leave resets them to 0, so the control
+// region is zero again when the launch ends (as every kernel leaves it).  All CTAs of a launch
+// must be co-resident (one per SM, grid <= SMs), as for the persistent kernels; a wait that
+// exceeds kWaitTimeoutNs aborts the launch (watchdog, TP_EWATCHDOG on the next call) instead of
+// hanging the GPU.
+#include "tp_ops.cuh"
+
+namespace tp {
+
+constexpr int kResMaxLocal = 3;           // blocks staged per CTA and row
+constexpr int kResMaxBuf = 7;             // rows staged per CTA (bf16 rows of one block per CTA)
+constexpr int kResSlots = 8;              // staged blocks per CTA (nbuf x nloc <= 7 for every dtype)
+constexpr int kResThreads = kThreads + 128;  // 16 compute warps + 4 service warps
+constexpr int kResMaxNb = kGroupBlocks;   // rows of at most one canonical group (one warp tree)
+constexpr int kResSmemMax = 227 * 1024 - 1792;  // dynamic shared memory (static arrays ~1.5 KB)
+
+template <typename In>
+constexpr int res_max_local() {  // blocks per row and CTA (at least two rows staged)
+    const int b = kResSmemMax / (2 * kBlockElems * (int)sizeof(In));
+    return b < kResMaxLocal ? b : kResMaxLocal;
+}
+// rows staged per CTA for shares of `per` blocks
+template <typename In>
+int res_nbuf(int per) {
+    int n = kResSmemMax / (per * kBlockElems * (int)sizeof(In));
+    if (n > kResMaxBuf) n = kResMaxBuf;
+    return n * per <= kResSlots ? n : kResSlots / per;
+}
+
+__device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Roles.  16 compute warps: pass 1 of rows 0 .. ahead-1; then per row k: pass 1 of row k+ahead,
+// pass 2 of row k (each warp arrives on a block's p1_bar after pass 1 and on its empty_bar after
+// reading the stage in pass 2).  Four service warps, none of which stores outputs (a release
+// then waits only for its own block value, not for a queue of streaming stores), each blocking
+// only on its own waits so that their latencies overlap: the post warp (block value = tree over
+// the 16 warp values, stored and released by the row ticket), two statistics warps (even / odd
+// rows: wait for the group's nb tickets, canonical tree, s_st + stats_bar), the load warp (stages rows in; refills a stage with the row
+// nbuf ahead once pass 2 has read it).  20 warps: the same 96-register cap as 17.
+constexpr int kResPostWarp = kWarps, kResStatsWarp = kWarps + 1, kResLoadWarp = kWarps + 3;
+
+template <typename In>
+__global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, int G, int ngroups, int nbuf, int ahead) {
+    constexpr int V = InTraits<In>::V;
+    constexpr int S = kResSlots;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    In* stages = reinterpret_cast<In*>(dsm);  // [nbuf][nloc] blocks; slot index b * nloc + j
+    __shared__ __align__(8) uint64_t full_bar[S];
+    __shared__ __align__(8) uint64_t p1_bar[S];
+    __shared__ __align__(8) uint64_t empty_bar[S];
+    __shared__ __align__(8) uint64_t stats_bar[S];
+    __shared__ Pair wparts[S][kWarps];
+    __shared__ unsigned char cbits[S][kWarps];
+    __shared__ float2 s_st[S];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nb = (int)a.nb;
+    const int grp = (int)blockIdx.x / G;
+    const int q = (int)blockIdx.x - grp * G;
+    const int nloc = (nb - q + G - 1) / G;  // this CTA's blocks: q + j * G, j < nloc
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(a.ws);
+    unsigned* err = &hdr->error;
+    if (grp >= ngroups) return;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full_bar[i], 1);
+            mbar_init(&p1_bar[i], kWarps);
+            mbar_init(&empty_bar[i], kWarps);
+            mbar_init(&stats_bar[i], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    pdl_wait_and_release();  // programmatic launch: touch memory only after the predecessor
+    publish_abort_word(a);
+    const int64_t nrows = (a.rows - grp + ngroups - 1) / ngroups;  // the group's rows: grp + k ngroups
+    auto slot = [&](int64_t k, int j) { return stages + ((size_t)(k % nbuf) * nloc + j) * kBlockElems; };
+    auto ph = [&](int64_t k) { return (uint32_t)((k / nbuf) & 1); };  // phase parity of row k's use
+    float2* bvals = reinterpret_cast<float2*>(a.ws + a.lay.block_vals);
+    unsigned* rt = reinterpret_cast<unsigned*>(a.ws + a.lay.row_tickets);
+
+    auto load_role = [&]() {  // ------------------------------------------------------ load warp
+        if (lane == 0) {
+            const In* x = static_cast<const In*>(a.x);
+            const uint64_t pol = policy_evict_first();  // every byte is read from HBM once
+            auto stage_in = [&](int64_t k, int j) {
+                const int64_t row = grp + k * ngroups;
+                const int64_t e0 = (int64_t)(q + j * G) * kBlockElems;
+                const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
+                uint64_t* fb = &full_bar[(k % nbuf) * nloc + j];
+                mbar_arrive_expect_tx(fb, bytes);
+                tma_load_1d(slot(k, j), x + row * a.cols + e0, bytes, fb, pol);
+            };
+            for (int64_t k = 0; k < nbuf && k < nrows; ++k)
+                for (int j = 0; j < nloc; ++j) stage_in(k, j);
+            for (int64_t k = 0; k + nbuf < nrows; ++k)
+                for (int j = 0; j < nloc; ++j) {  // pass 2 of row k has read the stage
+                    if (!wait_or_abort(&empty_bar[(k % nbuf) * nloc + j], ph(k), err, 2u)) return;
+                    fence_proxy_async_smem();
+                    stage_in(k + nbuf, j);
+                }
+        }
+    };
+    auto post_role = [&]() {  // ------------------------------------------------------ post warp
+        for (int64_t k = 0; k < nrows; ++k) {
+            const int b = (int)(k % nbuf);
+            const int64_t row = grp + k * ngroups;
+            for (int j = 0; j < nloc; ++j) {
+                if (!wait_or_abort(&p1_bar[b * nloc + j], ph(k), err, 32u)) return;
+                // block value: perfect tree over the 16 warp values in warp order (lanes 16-31
+                // identities: merge(v, identity) == v), as block_tree_warps
+                Pair v = lane < kWarps ? wparts[b * nloc + j][lane] : pair_identity();
+                v = warp_tree_pairs(v);
+                if (lane == 0) {
+                    bvals[row * a.nb + q + j * G] = make_float2(v.m, v.n);
+                    red_add_release_gpu(&rt[row], 1u);  // release: the block value before its ticket
+                }
+            }
+        }
+    };
+    auto stats_role = [&]() {  // ------------------------------------------------ statistics warps
+        for (int64_t k = warp - kResStatsWarp; k < nrows; k += 2) {
+            const int b = (int)(k % nbuf);
+            const int64_t row = grp + k * ngroups;
+            // every lane polls the ticket (one coalesced load) with acquire semantics, so each
+            // lane's loads of the block values below are ordered after its own acquire
+            const unsigned long long t0 = globaltimer_ns();
+            unsigned ns = 32;
+            while (!__all_sync(0xffffffffu, ld_acquire_gpu(&rt[row]) >= (unsigned)nb)) {
+                if (aborted(err)) return;
+                __nanosleep(ns);
+                ns = ns < 128 ? ns * 2 : ns;
+                if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                    if (lane == 0) raise_abort(err, 8u);
+                    return;
+                }
+            }
+            const float2* rv = bvals + row * a.nb;
+            const Pair root = warp_tree64(nb, [&](int j) {
+                const float2 f = __ldcg(rv + j);
+                return Pair{f.x, f.y};
+            });
+            if (lane == 0) {
+                s_st[b] = make_float2(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m));
+                mbar_arrive(&stats_bar[b]);
+            }
+        }
+    };
+
+    // ------------------------------------------------------------------------ compute warps
+    auto pass1 = [&](int64_t k) -> bool {  // pass 1 of this warp's share of row k
+        const int b = (int)(k % nbuf);
+        for (int j = 0; j < nloc; ++j) {
+            if (!wait_or_abort(&full_bar[b * nloc + j], ph(k), err, 4u)) return false;
+            const int valid = (int)min((int64_t)kBlockElems, a.cols - (int64_t)(q + j * G) * kBlockElems);
+            BlockVals v;
+            load_stage<In>(slot(k, j), v);
+            Pair wp;
+            const bool cl = warp_pass1<V>(v, valid, &wp);
+            if (lane == 0) {
+                wparts[b * nloc + j][warp] = wp;
+                cbits[b * nloc + j][warp] = cl ? 1 : 0;
+                mbar_arrive(&p1_bar[b * nloc + j]);  // release: the warp value before the arrival
+            }
+        }
+        return true;
+    };
+    // pass 1 runs `ahead` rows before pass 2: the group exchange of row k (the slowest CTA of the
+    // group, the ticket round trips, the row tree) hides behind pass 1 of rows k+1 .. k+ahead,
+    // and nbuf - 1 - ahead rows are in flight from HBM
+    auto compute_role = [&]() {
+        for (int64_t k = 0; k < ahead && k < nrows; ++k)
+            if (!pass1(k)) return;
+        for (int64_t k = 0; k < nrows; ++k) {
+            if (k + ahead < nrows && !pass1(k + ahead)) return;
+            const int b = (int)(k % nbuf);
+            if (!wait_or_abort(&stats_bar[b], ph(k), err, 16u)) return;
+            const float4 st = make_float4(s_st[b].x, s_st[b].y, 0.f, 0.f);
+            const int64_t row = grp + k * ngroups;
+            for (int j = 0; j < nloc; ++j) {  // pass 2 on the staged blocks
+                const int64_t e0 = (int64_t)(q + j * G) * kBlockElems;
+                const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
+                BlockVals v;
+                load_stage<In>(slot(k, j), v);
+                const bool clamp = cbits[b * nloc + j][warp] != 0;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[b * nloc + j]);  // the stage may take the row nbuf ahead
+                op_pass2<V>(v, st, clamp, a.y + row * a.cols + e0, valid, true);
+            }
+        }
+    };
+
+    if (warp < kWarps) compute_role();
+    else if (warp == kResPostWarp) post_role();
+    else if (warp == kResLoadWarp) load_role();
+    else stats_role();
+    // Every role returns here (also on a watchdog abort).  The last CTA out resets the row tickets
+    // (posts and reads are counted, never reset, during the launch: no reader ever waits on a
+    // returning atomic) and advances the workspace epoch, as exit_and_reset.
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&hdr->exit_ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int64_t r = threadIdx.x; r < a.rows; r += blockDim.x) rt[r] = 0u;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            hdr->counter = 0ull;
+            hdr->exit_ticket = 0u;
+            __threadfence();
+            atomicAdd(&hdr->epoch, 1u);
+        }
+    }
+}
+
+// CTAs per row (G) for rows x nb blocks on `sms` SMs, 0 when the schedule does not apply.
+// Forced (force_g > 0): any G whose share ceil(nb / G) fits the stages (rows of 4..64 blocks).
+// Automatic: one block per CTA and row (G = nb), where the stages hold >= 5 rows, i.e. bf16 rows
+// (7 rows of 32 KB): the exchange of a row over G CTAs needs several rows of slack under full HBM
+// load (measured, C4 bf16: G = 49 with 7 rows staged 293 us, against the cluster kernel's 318 us
+// in the same run; G = 17 / 25 with 2 / 3 rows staged 347-450 us).  fp32 rows stage only 3 blocks
+// per SM, too little slack: C4 fp32 424 us against 350 us; they stay on the cluster kernel.  At
+// least two rows per group, so that the rows' exchanges overlap.
+template <typename In>
+int rowres_choose(int64_t rows, int64_t nb, int sms, int force_g) {
+    constexpr int B = res_max_local<In>();
+    if (nb < 4 || nb > kResMaxNb || rows < 1) return 0;
+    const int gmin = (int)((nb + B - 1) / B);
+    if (force_g > 0) return force_g >= gmin && force_g <= nb && force_g <= sms ? force_g : 0;
+    if (res_nbuf<In>(1) < 5 || nb > sms || rows < 2 * (sms / nb)) return 0;
+    return (int)nb;
+}
+
+template <typename In>
+cudaError_t launch_rowres(KArgs a, int G, const LaunchOpts& o, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sms = device_sms(dev);
+    if (G < 1 || a.nb > kResMaxNb || (a.nb + G - 1) / G > res_max_local<In>() || !a.ws) return cudaErrorNotSupported;
+    int64_t ngroups = (o.grid_ctas > 0 ? o.grid_ctas : sms) / G;
+    if (ngroups > a.rows) ngroups = a.rows;
+    if (ngroups < 1) return cudaErrorNotSupported;
+    const int per = (int)((a.nb + G - 1) / G);
+    const int nbuf = res_nbuf<In>(per);
+    const size_t dyn = (size_t)nbuf * per * kBlockElems * sizeof(In);
+    static DevCache configured[kMaxDevices];
+    if (!configured[dev].load(std::memory_order_acquire)) {
+        cudaFuncSetAttribute(rowres_kernel<In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kResSmemMax);
+        configured[dev].store(1, std::memory_order_release);
+    }
+    // pass 1 ahead of pass 2 by `ahead` rows, the other staged rows in flight (measured on C4
+    // bf16, nbuf 7: ahead 3 / 4 / 5 / 6 = 337 / 332 / 335 / 358 us; the exchange's latency under
+    // full HBM load needs the slack more than the loads need depth)
+    int ahead = nbuf >= 5 ? nbuf - 3 : (nbuf > 1 ? nbuf - 1 : 1);
+    if (o.lookahead_rows > 0 && o.lookahead_rows < nbuf) ahead = (int)o.lookahead_rows;
+    last_plan() = Plan{6, kTwoPass, ngroups * G, G, ahead, nbuf};  // lookahead_rows: pass-1 lead; hold: rows staged
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(ngroups * G));
+    cfg.blockDim = dim3(kResThreads);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, rowres_kernel<In>, a, G, (int)ngroups, nbuf, ahead);
+}
+
+template int rowres_choose<float>(int64_t, int64_t, int, int);
+template int rowres_choose<uint16_t>(int64_t, int64_t, int, int);
+template cudaError_t launch_rowres<float>(KArgs, int, const LaunchOpts&, cudaStream_t);
+template cudaError_t launch_rowres<uint16_t>(KArgs, int, const LaunchOpts&, cudaStream_t);
+
+}  // namespace tp

@@ -316,6 +316,71 @@ def test_small_schedule_agrees_bitwise(rows, cols, dtype):
         assert_parity(x[1:], y[1:], "small")
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,cols", [(5, 16384 * 4), (3, 16384 * 64), (40, 16384 * 7 + 8), (300, 16384 * 5 + 4000),
+                                       (24, 16384 * 49 + 5000)])
+def test_resident_schedule_agrees_bitwise(rows, cols, dtype):
+    # a group of CTAs per row stages its whole share, exchanges block values through the
+    # workspace tickets, pass 2 on the staged blocks (tp_rowres.cu): the same canonical trees as
+    # the stream kernel, so the same bits; forced group sizes and capped grids make groups loop
+    # over many rows (ticket reuse per row, stage refills across rows); clamped blocks (G11)
+    x = workloads.ragged_case(rows, cols, -400, 400, seed=21, stream=rows + cols)
+    x[0, 5] = 4.0e7
+    x[rows - 1, cols - 3] = -2.0e9
+    if dtype == "bf16":
+        x = workloads.to_bf16(x)
+    xd = to_dev(x)
+    ws = tp.new_workspace(rows, cols)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM, workspace=ws))
+    nb = -(-cols // 16384)
+    bmax = 3 if dtype == "bf16" else 1
+    gmin = -(-nb // bmax)
+    y = to_host(tp.softmax_ex(xd, workspace=ws))  # AUTO: bf16 rows of one block per CTA take it
+    assert np.array_equal(ref, y)
+    if dtype == "bf16" and rows >= 2 * (148 // nb):
+        assert tp.last_plan()["kernel"] == "resident"
+    ran = 0
+    for g, grid in ((0, 0), (gmin, 0), (min(nb, gmin + 1), 0), (gmin, 2 * gmin), (nb, 0), (gmin, gmin)):
+        for rep in range(2):  # the same workspace twice: tickets left at zero by each launch
+            y = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_RESIDENT, cluster_size=g, grid_ctas=grid, workspace=ws))
+            assert tp.watchdog_flags(ws) == 0
+            assert np.array_equal(ref, y), (g, grid, rep)
+        ran += tp.last_plan()["kernel"] == "resident"
+    assert ran >= 5
+    # a stream launch on the same workspace afterwards (control region shared): still the same
+    assert np.array_equal(ref, to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM, workspace=ws)))
+    if rows * cols <= 3_000_000:
+        assert_parity(x, ref, "resident")
+    else:
+        assert_parity(x[:2], ref[:2], "resident")
+
+
+def test_resident_schedule_graph_capture_and_streams():
+    # the resident-row launch inside a CUDA graph, replayed; and two workspaces on two streams
+    x = workloads.to_bf16(workloads.ragged_case(64, 16384 * 20 + 304, -300, 300, seed=22, stream=22))
+    xd = to_dev(x)
+    ref = to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM))
+    ws = tp.new_workspace(*x.shape)
+    y = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+    tp.softmax_ex(xd, out=y, workspace=ws)
+    assert tp.last_plan()["kernel"] == "resident"
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        tp.softmax_ex(xd, out=y, workspace=ws)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            tp.softmax_ex(xd, out=y, workspace=ws)
+    for _ in range(3):
+        y.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(ref, to_host(y))
+    assert tp.watchdog_flags(ws) == 0
+    assert_parity(x[:3], ref[:3], "resident graph")
+
+
 def test_cluster_schedule_clamped_blocks_and_small_grids():
     # out-of-domain blocks (reading G11) inside multi-block rows: the per-warp clamp masks stay
     # local to the CTA that ran pass 1; a capped grid makes clusters loop over many rows
