@@ -65,7 +65,9 @@ __host__ __device__ inline size_t mailbox_flag_offset(unsigned epoch, int rank) 
 constexpr unsigned long long kWaitTimeoutNs = 4000000000ull;  // 4 s: only a bug can wait this long
 
 struct WsLayout {
-    size_t group_tickets, row_tickets, row_ready, row_clamp, ctrl_bytes;  // control region [0, ctrl_bytes)
+    size_t group_tickets, row_tickets, row_ready, row_clamp;  // control region [0, ctrl_bytes)
+    size_t res_vals;  // resident-row kernel: epoch-tagged block values, 16 B per (row, block)
+    size_t ctrl_bytes;
     size_t row_stats, block_vals, block_clamp, group_vals, bytes;  // data region
 };
 

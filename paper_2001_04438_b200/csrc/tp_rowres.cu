@@ -19,14 +19,17 @@
 // warp), block tree over the 16 warp values, canonical tree over the row's blocks (one group of
 // nb <= 64 leaves, warp_tree64 as tp_rowcl.cu's cl_row_stats) and pass 2 (op_pass2).
 //
-// Group exchange (global memory, workspace): each block value is stored into the row's
-// block_vals and released by the row ticket (red.release, one per block); a CTA's statistics warp
-// polls the ticket until it reaches nb (acquire), forms the row statistics from the nb values.
-// Tickets only count up during a launch; the last CTA to leave resets them to 0, so the control
-// region is zero again when the launch ends (as every kernel leaves it).  All CTAs of a launch
-// must be co-resident (one per SM, grid <= SMs), as for the persistent kernels; a wait that
-// exceeds kWaitTimeoutNs aborts the launch (watchdog, TP_EWATCHDOG on the next call) instead of
-// hanging the GPU.
+// Group exchange (global memory, workspace control region `res_vals`): each block value is
+// stored as two 64-bit words, bits(m) and bits(n), each with the launch's tag (workspace epoch +
+// 1) in its upper half; a CTA's statistics warp loads the row's nb slots until every word carries
+// the tag (single-copy-atomic 64-bit accesses: a tagged word is a complete value), then forms the
+// row statistics.  The first version released each value by a row ticket (red.release) and
+// polled the ticket: two round trips to L2 per row under full HBM load instead of one
+// (C4 bf16 ~300 us).  The last CTA out advances the epoch; the control region (tags included)
+// is zeroed whenever a workspace changes shape, which also resets the epoch.  All CTAs of a
+// launch must be co-resident (one per SM, grid <= SMs), as for the persistent kernels; a wait
+// that exceeds kWaitTimeoutNs aborts the launch (watchdog, TP_EWATCHDOG on the next call)
+// instead of hanging the GPU.
 #include "tp_ops.cuh"
 
 namespace tp {
@@ -51,8 +54,13 @@ int res_nbuf(int per) {
     return n * per <= kResSlots ? n : kResSlots / per;
 }
 
-__device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // Roles.  16 compute warps: pass 1 of rows 0 .. ahead-1; then per row k: pass 1 of row k+ahead,
@@ -60,8 +68,8 @@ __device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
 // reading the stage in pass 2).  Four service warps, none of which stores outputs (a release
 // then waits only for its own block value, not for a queue of streaming stores), each blocking
 // only on its own waits so that their latencies overlap: the post warp (block value = tree over
-// the 16 warp values, stored and released by the row ticket), two statistics warps (even / odd
-// rows: wait for the group's nb tickets, canonical tree, s_st + stats_bar), the load warp (stages rows in; refills a stage with the row
+// the 16 warp values, stored as tagged words), two statistics warps (even / odd
+// rows: wait for the group's nb tagged values, canonical tree, s_st + stats_bar), the load warp (stages rows in; refills a stage with the row
 // nbuf ahead once pass 2 has read it).  20 warps: the same 96-register cap as 17.
 constexpr int kResPostWarp = kWarps, kResStatsWarp = kWarps + 1, kResLoadWarp = kWarps + 3;
 
@@ -98,11 +106,15 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
     __syncthreads();
     pdl_wait_and_release();  // programmatic launch: touch memory only after the predecessor
     publish_abort_word(a);
+    __shared__ unsigned s_epoch;
+    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
+    __syncthreads();
+    const unsigned long long tag = (unsigned long long)(s_epoch + 1u) << 32;  // this launch's tag
     const int64_t nrows = (a.rows - grp + ngroups - 1) / ngroups;  // the group's rows: grp + k ngroups
     auto slot = [&](int64_t k, int j) { return stages + ((size_t)(k % nbuf) * nloc + j) * kBlockElems; };
     auto ph = [&](int64_t k) { return (uint32_t)((k / nbuf) & 1); };  // phase parity of row k's use
-    float2* bvals = reinterpret_cast<float2*>(a.ws + a.lay.block_vals);
-    unsigned* rt = reinterpret_cast<unsigned*>(a.ws + a.lay.row_tickets);
+    // block value slots: (bits(m) | tag, bits(n) | tag), two single-copy-atomic 64-bit words
+    unsigned long long* slots = reinterpret_cast<unsigned long long*>(a.ws + a.lay.res_vals);
 
     auto load_role = [&]() {  // ------------------------------------------------------ load warp
         if (lane == 0) {
@@ -136,9 +148,10 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
                 // identities: merge(v, identity) == v), as block_tree_warps
                 Pair v = lane < kWarps ? wparts[b * nloc + j][lane] : pair_identity();
                 v = warp_tree_pairs(v);
-                if (lane == 0) {
-                    bvals[row * a.nb + q + j * G] = make_float2(v.m, v.n);
-                    red_add_release_gpu(&rt[row], 1u);  // release: the block value before its ticket
+                if (lane == 0) {  // each word carries the launch's tag: no flag, no fence
+                    unsigned long long* w = slots + 2 * (row * a.nb + q + j * G);
+                    st_relaxed_gpu_u64(w, tag | __float_as_uint(v.m));
+                    st_relaxed_gpu_u64(w + 1, tag | __float_as_uint(v.n));
                 }
             }
         }
@@ -147,11 +160,27 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
         for (int64_t k = warp - kResStatsWarp; k < nrows; k += 2) {
             const int b = (int)(k % nbuf);
             const int64_t row = grp + k * ngroups;
-            // every lane polls the ticket (one coalesced load) with acquire semantics, so each
-            // lane's loads of the block values below are ordered after its own acquire
+            // every lane loads its leaves' tagged words until all of the row's nb carry this
+            // launch's tag: the poll is the load of the values (one round trip once they are in)
+            const unsigned long long* rw = slots + 2 * row * a.nb;
+            const int l0 = nb > 32 ? 2 * lane : lane, l1 = l0 + 1;
+            const bool has0 = l0 < nb, has1 = nb > 32 && l1 < nb;
+            Pair p0 = pair_identity(), p1 = pair_identity();
             const unsigned long long t0 = globaltimer_ns();
             unsigned ns = 32;
-            while (!__all_sync(0xffffffffu, ld_acquire_gpu(&rt[row]) >= (unsigned)nb)) {
+            for (;;) {
+                bool ok = true;
+                if (has0) {
+                    const unsigned long long m = ld_relaxed_gpu_u64(rw + 2 * l0), n = ld_relaxed_gpu_u64(rw + 2 * l0 + 1);
+                    ok = ((m ^ tag) >> 32) == 0 && ((n ^ tag) >> 32) == 0;
+                    p0 = Pair{__uint_as_float((unsigned)m), __uint_as_float((unsigned)n)};
+                }
+                if (has1) {
+                    const unsigned long long m = ld_relaxed_gpu_u64(rw + 2 * l1), n = ld_relaxed_gpu_u64(rw + 2 * l1 + 1);
+                    ok = ok && ((m ^ tag) >> 32) == 0 && ((n ^ tag) >> 32) == 0;
+                    p1 = Pair{__uint_as_float((unsigned)m), __uint_as_float((unsigned)n)};
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
                 if (aborted(err)) return;
                 __nanosleep(ns);
                 ns = ns < 128 ? ns * 2 : ns;
@@ -160,11 +189,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
                     return;
                 }
             }
-            const float2* rv = bvals + row * a.nb;
-            const Pair root = warp_tree64(nb, [&](int j) {
-                const float2 f = __ldcg(rv + j);
-                return Pair{f.x, f.y};
-            });
+            const Pair root = warp_tree64(nb, [&](int j) { return j == l0 ? p0 : p1; });
             if (lane == 0) {
                 s_st[b] = make_float2(__fsub_rn(root.n, 1.0f), __fdiv_rn(0.5f, root.m));
                 mbar_arrive(&stats_bar[b]);
@@ -191,7 +216,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
         return true;
     };
     // pass 1 runs `ahead` rows before pass 2: the group exchange of row k (the slowest CTA of the
-    // group, the ticket round trips, the row tree) hides behind pass 1 of rows k+1 .. k+ahead,
+    // group, the round trip to L2, the row tree) hides behind pass 1 of rows k+1 .. k+ahead,
     // and nbuf - 1 - ahead rows are in flight from HBM
     auto compute_role = [&]() {
         for (int64_t k = 0; k < ahead && k < nrows; ++k)
@@ -219,27 +244,10 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
     else if (warp == kResPostWarp) post_role();
     else if (warp == kResLoadWarp) load_role();
     else stats_role();
-    // Every role returns here (also on a watchdog abort).  The last CTA out resets the row tickets
-    // (posts and reads are counted, never reset, during the launch: no reader ever waits on a
-    // returning atomic) and advances the workspace epoch, as exit_and_reset.
+    // Every role returns here (also on a watchdog abort): the last CTA out advances the workspace
+    // epoch (exit_and_reset), so the next launch's tag differs from every tag written here.
     __syncthreads();
-    __shared__ int s_last;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&hdr->exit_ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        for (int64_t r = threadIdx.x; r < a.rows; r += blockDim.x) rt[r] = 0u;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            hdr->counter = 0ull;
-            hdr->exit_ticket = 0u;
-            __threadfence();
-            atomicAdd(&hdr->epoch, 1u);
-        }
-    }
+    if (threadIdx.x == 0) exit_and_reset(hdr);
 }
 
 // CTAs per row (G) for rows x nb blocks on `sms` SMs, 0 when the schedule does not apply.

@@ -30,6 +30,9 @@ __host__ __device__ inline WsLayout ws_layout(int64_t rows, int64_t cols) {
     L.row_tickets = off;   off = align256(off + sizeof(unsigned) * rows);
     L.row_ready = off;     off = align256(off + sizeof(unsigned) * rows * 2);
     L.row_clamp = off;     off = align256(off + sizeof(unsigned) * rows);
+    // in the control region: zero-filled with the header on a shape change, so that no tag of a
+    // previous shape's launch can equal a tag of this shape's epochs (tp_rowres.cu)
+    L.res_vals = off;      off = align256(off + 16 * rows * (nb <= kGroupBlocks ? nb : 0));
     L.ctrl_bytes = off;
     L.row_stats = off;     off = align256(off + sizeof(float4) * rows * 2);
     L.block_vals = off;    off = align256(off + sizeof(float2) * rows * nb);
