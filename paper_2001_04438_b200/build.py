@@ -9,8 +9,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libtwopass.so")
-SOURCES = ["tp_kernels.cu", "tp_stream.cu", "tp_rowcl.cu", "tp_rowcl3.cu", "tp_small.cu", "tp_rowph.cu", "tp_rowres.cu", "tp_peer.cu", "tp_api.cu", "tp_debug.cu"]
-HEADERS = ["tp_common.cuh", "tp_block.cuh", "tp_sched.cuh", "tp_ops.cuh", "tp_internal.h"]
+SOURCES = ["tp_kernels.cu", "tp_stream.cu", "tp_rowcl.cu", "tp_rowcl3.cu", "tp_small.cu", "tp_rowph.cu", "tp_rowres.cu", "tp_rowres3.cu", "tp_peer.cu", "tp_api.cu", "tp_debug.cu"]
+HEADERS = ["tp_rowres.cuh", "tp_common.cuh", "tp_block.cuh", "tp_sched.cuh", "tp_ops.cuh", "tp_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

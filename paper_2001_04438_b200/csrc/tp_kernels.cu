@@ -318,12 +318,17 @@ static cudaError_t launch_algo(const void* x, float* y, int64_t rows, int64_t co
             return launch_small<In, (A == kFused ? kTwoPass : A)>(a, o, s);
         // Two-Pass rows whose share fits shared memory: a group of CTAs per row, the row read
         // once (tp_rowres.cu)
-        if (A == kTwoPass && (o.schedule == 6 || (o.schedule == 0 && rowres_auto<In>()))) {
+        // (the Three-Pass comparators too, so that they are compared on the same footing; AUTO
+        // for Recompute, not for Reload, whose third pass re-reads Y from memory anyway:
+        // C4 bf16 Recompute 442 -> 385 us, Reload 599 -> 711 us)
+        if ((A == kTwoPass || A == kRecompute || A == kReload) &&
+            (o.schedule == 6 || (o.schedule == 0 && A != kReload && rowres_auto<In>()))) {
             int dev = 0;
             cudaGetDevice(&dev);
             const int G = rowres_choose<In>(a.rows, a.nb, device_sms(dev), o.cluster_size);
             if (G) {
-                const cudaError_t e = launch_rowres<In>(a, G, o, s);
+                const cudaError_t e = A == kTwoPass ? launch_rowres<In>(a, G, o, s)
+                                                     : launch_rowres3<In, (A == kReload ? kReload : kRecompute)>(a, G, o, s);
                 if (e != cudaErrorNotSupported) return e;
                 cudaGetLastError();
             }

@@ -321,5 +321,7 @@ template <typename In>
 int rowres_choose(int64_t rows, int64_t nb, int sms, int force_g);
 template <typename In>
 cudaError_t launch_rowres(KArgs a, int G, const LaunchOpts& o, cudaStream_t s);
+template <typename In, int A>
+cudaError_t launch_rowres3(KArgs a, int G, const LaunchOpts& o, cudaStream_t s);
 
 }  // namespace tp

@@ -30,38 +30,9 @@
 // launch must be co-resident (one per SM, grid <= SMs), as for the persistent kernels; a wait
 // that exceeds kWaitTimeoutNs aborts the launch (watchdog, TP_EWATCHDOG on the next call)
 // instead of hanging the GPU.
-#include "tp_ops.cuh"
+#include "tp_rowres.cuh"
 
 namespace tp {
-
-constexpr int kResMaxLocal = 3;           // blocks staged per CTA and row
-constexpr int kResMaxBuf = 7;             // rows staged per CTA (bf16 rows of one block per CTA)
-constexpr int kResSlots = 8;              // staged blocks per CTA (nbuf x nloc <= 7 for every dtype)
-constexpr int kResThreads = kThreads + 128;  // 16 compute warps + 4 service warps
-constexpr int kResMaxNb = kGroupBlocks;   // rows of at most one canonical group (one warp tree)
-constexpr int kResSmemMax = 227 * 1024 - 1792;  // dynamic shared memory (static arrays ~1.5 KB)
-
-template <typename In>
-constexpr int res_max_local() {  // blocks per row and CTA (at least two rows staged)
-    const int b = kResSmemMax / (2 * kBlockElems * (int)sizeof(In));
-    return b < kResMaxLocal ? b : kResMaxLocal;
-}
-// rows staged per CTA for shares of `per` blocks
-template <typename In>
-int res_nbuf(int per) {
-    int n = kResSmemMax / (per * kBlockElems * (int)sizeof(In));
-    if (n > kResMaxBuf) n = kResMaxBuf;
-    return n * per <= kResSlots ? n : kResSlots / per;
-}
-
-__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // Roles.  16 compute warps: pass 1 of rows 0 .. ahead-1; then per row k: pass 1 of row k+ahead,
 // pass 2 of row k (each warp arrives on a block's p1_bar after pass 1 and on its empty_bar after
@@ -71,7 +42,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
 // the 16 warp values, stored as tagged words), two statistics warps (even / odd
 // rows: wait for the group's nb tagged values, canonical tree, s_st + stats_bar), the load warp (stages rows in; refills a stage with the row
 // nbuf ahead once pass 2 has read it).  20 warps: the same 96-register cap as 17.
-constexpr int kResPostWarp = kWarps, kResStatsWarp = kWarps + 1, kResLoadWarp = kWarps + 3;
 
 template <typename In>
 __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, int G, int ngroups, int nbuf, int ahead) {
@@ -280,18 +250,33 @@ cudaError_t launch_rowres(KArgs a, int G, const LaunchOpts& o, cudaStream_t s) {
     const int per = (int)((a.nb + G - 1) / G);
     const int nbuf = res_nbuf<In>(per);
     const size_t dyn = (size_t)nbuf * per * kBlockElems * sizeof(In);
+    constexpr int A = kTwoPass;
+    auto kern = rowres_kernel<In>;
     static DevCache configured[kMaxDevices];
     if (!configured[dev].load(std::memory_order_acquire)) {
-        cudaFuncSetAttribute(rowres_kernel<In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kResSmemMax);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
         configured[dev].store(1, std::memory_order_release);
     }
-    // pass 1 ahead of pass 2 by `ahead` rows, the other staged rows in flight (measured on C4
-    // bf16, nbuf 7: ahead 3 / 4 / 5 / 6 = 337 / 332 / 335 / 358 us; the exchange's latency under
-    // full HBM load needs the slack more than the loads need depth)
-    int ahead = nbuf >= 5 ? nbuf - 3 : (nbuf > 1 ? nbuf - 1 : 1);
-    if (o.lookahead_rows > 0 && o.lookahead_rows < nbuf) ahead = (int)o.lookahead_rows;
-    last_plan() = Plan{6, kTwoPass, ngroups * G, G, ahead, nbuf};  // lookahead_rows: pass-1 lead; hold: rows staged
+    // Two-Pass: pass 1 ahead of pass 2 by `ahead` rows, the other staged rows in flight (measured
+    // on C4 bf16, nbuf 7: ahead 3 / 4 / 5 / 6 = 337 / 332 / 335 / 358 us; the exchange's latency
+    // under full HBM load needs the slack more than the loads need depth).  Three-Pass: each pass
+    // `ahead` rows behind the previous one; Recompute keeps 2 ahead + 1 rows staged, Reload
+    // ahead + 1.
+    int ahead, lim;
+    if (A == kTwoPass) {
+        ahead = nbuf >= 5 ? nbuf - 3 : (nbuf > 1 ? nbuf - 1 : 1);
+        lim = nbuf - 1;
+    } else if (A == kRecompute) {
+        ahead = nbuf >= 5 ? 2 : 1;
+        lim = (nbuf - 1) / 2;
+    } else {
+        ahead = nbuf >= 5 ? 3 : 1;
+        lim = nbuf - 1;
+    }
+    if (lim < 1) return cudaErrorNotSupported;
+    if (o.lookahead_rows > 0 && o.lookahead_rows <= lim) ahead = (int)o.lookahead_rows;
+    if (ahead > lim) ahead = lim;
+    last_plan() = Plan{6, A, ngroups * G, G, ahead, nbuf};  // lookahead_rows: rows between passes; hold: rows staged
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(ngroups * G));
     cfg.blockDim = dim3(kResThreads);
@@ -302,7 +287,7 @@ cudaError_t launch_rowres(KArgs a, int G, const LaunchOpts& o, cudaStream_t s) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, rowres_kernel<In>, a, G, (int)ngroups, nbuf, ahead);
+    return cudaLaunchKernelEx(&cfg, kern, a, G, (int)ngroups, nbuf, ahead);
 }
 
 template int rowres_choose<float>(int64_t, int64_t, int, int);

@@ -349,6 +349,16 @@ def test_resident_schedule_agrees_bitwise(rows, cols, dtype):
     assert ran >= 5
     # a stream launch on the same workspace afterwards (control region shared): still the same
     assert np.array_equal(ref, to_host(tp.softmax_ex(xd, schedule=tp.SCHED_STREAM, workspace=ws)))
+    # the Three-Pass comparators on the same schedule: bitwise equal to their stream-kernel runs
+    for algo in ("recompute", "reload"):
+        ref3 = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_STREAM, workspace=ws))
+        for g, grid in ((0, 0), (nb, 0), (gmin, 0), (gmin, gmin)):
+            y3 = to_host(tp.softmax_ex(xd, ALGOS[algo], schedule=tp.SCHED_RESIDENT, cluster_size=g, grid_ctas=grid,
+                                       workspace=ws))
+            assert tp.watchdog_flags(ws) == 0
+            assert np.array_equal(ref3, y3), (algo, g, grid)
+        if rows * cols <= 3_000_000:
+            assert_parity(x[1:], ref3[1:], f"resident {algo}")
     if rows * cols <= 3_000_000:
         assert_parity(x, ref, "resident")
     else:

@@ -19,7 +19,7 @@ for cfg in c5 c4 c4b c3 c2; do
     --clock-control none --csv --log-file $out/${tag}_traffic_$cfg.csv python tools/prof_run.py --config $cfg --iters 4 \
     > $out/${tag}_ncu_traffic_$cfg.log 2>&1
 done
-for spec in "c5 rowph 1" "c4b rowres 2"; do
+for spec in "c5 rowph 1" "c4b rowres 1"; do
   set -- $spec
   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 \
     -o $out/${tag}_full_$1 python tools/prof_run.py --config $1 --iters 2 > $out/${tag}_ncu_full_$1.log 2>&1

@@ -36,7 +36,9 @@ def main():
     ap.add_argument("--groups", default="0")
     ap.add_argument("--only-resident", action="store_true")
     ap.add_argument("--ahead", default="0")
+    ap.add_argument("--algo", default="two_pass", choices=["two_pass", "recompute", "reload"])
     args = ap.parse_args()
+    algo = {"two_pass": tp.ALGO_TWO_PASS, "recompute": tp.ALGO_RECOMPUTE, "reload": tp.ALGO_RELOAD}[args.algo]
     for key in args.configs.split(","):
         cfg = workloads.CONFIGS[key]
         x = workloads.generate(key)
@@ -53,17 +55,17 @@ def main():
         scheds += [(f"resident_g{g}_a{la}", tp.SCHED_RESIDENT, int(g), int(la)) for g in args.groups.split(",")
                    for la in args.ahead.split(",")]
         for name, sc, g, la in scheds:
-            tp.softmax_ex(xd, out=y, workspace=ws, schedule=sc, cluster_size=g, lookahead_rows=la)
+            tp.softmax_ex(xd, algo, out=y, workspace=ws, schedule=sc, cluster_size=g, lookahead_rows=la)
             torch.cuda.synchronize()
             plan = tp.last_plan()
             h = y.cpu().numpy()
             if ref is None:
                 ref = h.copy()
             same = bool(np.array_equal(ref, h))
-            us = timed(lambda: tp.softmax_ex(xd, out=y, workspace=ws, schedule=sc, cluster_size=g, lookahead_rows=la),
+            us = timed(lambda: tp.softmax_ex(xd, algo, out=y, workspace=ws, schedule=sc, cluster_size=g, lookahead_rows=la),
                        args.reps)
             gbs = BYTES[cfg.dtype] * cfg.elements / (us * 1e-6) / 1e9
-            print(json.dumps(dict(config=key, sched=name, plan=plan, us=us, alg_GBps=gbs, bitwise_vs_stream=same,
+            print(json.dumps(dict(config=key, algo=args.algo, sched=name, plan=plan, us=us, alg_GBps=gbs, bitwise_vs_stream=same,
                                   watchdog=tp.watchdog_flags(ws))), flush=True)
 
 

@@ -19,7 +19,7 @@ import paper_2001_04438_b200 as tp  # noqa: E402
 import workloads  # noqa: E402
 from gpu_helpers import assert_parity  # noqa: E402
 
-SCHEDS = [tp.SCHED_AUTO, tp.SCHED_CLUSTER, tp.SCHED_SMALL, tp.SCHED_HOLD, tp.SCHED_PHASE]
+SCHEDS = [tp.SCHED_AUTO, tp.SCHED_CLUSTER, tp.SCHED_SMALL, tp.SCHED_HOLD, tp.SCHED_PHASE, tp.SCHED_RESIDENT]
 
 
 def main():
@@ -40,6 +40,8 @@ def main():
         algo = int(rng.choice([tp.ALGO_TWO_PASS, tp.ALGO_RECOMPUTE, tp.ALGO_RELOAD]))
         sched = int(rng.choice(SCHEDS))
         cl = int(rng.choice([0, 1, 2, 4, 8]))
+        if sched == tp.SCHED_RESIDENT:  # CTAs per row: automatic, one block each, or 2-3 blocks each
+            cl = int(rng.choice([0, nb, -(-nb // 3), -(-nb // 2), -(-nb // 3) + 1]))
         grid = int(rng.choice([0, 0, 0, 7, 33]))
         x = workloads.ragged_case(rows, cols, -400.0, 400.0, seed=n, stream=7)
         if rng.random() < args.clamp_frac:  # out of domain: the clamped path, in a few rows

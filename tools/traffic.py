@@ -16,9 +16,9 @@ import json
 import os
 import sys
 
-OURS = ("stream_kernel", "rowcl_kernel", "rowph_kernel", "small_kernel", "general_kernel")
+OURS = ("stream_kernel", "rowcl_kernel", "rowph_kernel", "small_kernel", "general_kernel", "rowres_kernel")
 KNAME = {"c5": "tp::rowph_kernel<float,kTwoPass>", "c3": "tp::stream_kernel<float,kTwoPass>",
-         "c4": "tp::rowcl_kernel<float>", "c4b": "tp::rowcl_kernel<uint16_t>", "c2": "tp::small_kernel<float>"}
+         "c4": "tp::rowcl_kernel<float>", "c4b": "tp::rowres_kernel<uint16_t>", "c2": "tp::small_kernel<float>"}
 ALG = {"c5": 12 * 2 ** 31, "c3": 12 * 2 ** 26, "c4": 12 * 256 * 800000, "c4b": 8 * 256 * 800000,
        "c2": 12 * 64 * 32768}
 
