@@ -32,7 +32,20 @@
 // instead of hanging the GPU.
 #include "tp_rowres.cuh"
 
+#ifndef TP_RES_UNROLL
+#define TP_RES_UNROLL 1
+#endif
+#ifndef TP_RES_FUSE
+#define TP_RES_FUSE 1
+#endif
+#ifndef TP_RES_EXP
+#define TP_RES_EXP 0  // development timing experiments (wrong outputs for 2, 4, 8): never set in a release build
+#endif
+
 namespace tp {
+
+constexpr bool kResFuse = TP_RES_FUSE != 0;
+constexpr int kResUnroll = TP_RES_UNROLL;
 
 // Roles.  16 compute warps: pass 1 of rows 0 .. ahead-1; then per row k: pass 1 of row k+ahead,
 // pass 2 of row k (each warp arrives on a block's p1_bar after pass 1 and on its empty_bar after
@@ -42,6 +55,58 @@ namespace tp {
 // the 16 warp values, stored as tagged words), two statistics warps (even / odd
 // rows: wait for the group's nb tagged values, canonical tree, s_st + stats_bar), the load warp (stages rows in; refills a stage with the row
 // nbuf ahead once pass 2 has read it).  20 warps: the same 96-register cap as 17.
+
+
+// 8 consecutive values of this thread (group g of pass1_thread: BlockVals v[8 g .. 8 g + 7]) from a staged block.
+template <typename In>
+__device__ __forceinline__ void load_group8(const In* stage, int g, float (&x)[8]) {
+    constexpr int V = InTraits<In>::V;
+    if constexpr (V == 8) {
+        unpack_bf16x8(*reinterpret_cast<const uint4*>(stage + vec_off<8>((int)threadIdx.x, g)), x);
+    } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 a = *reinterpret_cast<const float4*>(stage + vec_off<4>((int)threadIdx.x, 2 * g + h));
+            x[4 * h] = a.x; x[4 * h + 1] = a.y; x[4 * h + 2] = a.z; x[4 * h + 3] = a.w;
+        }
+    }
+}
+
+// Pass 2 of one whole, unclamped staged block (s2 -> yb) and pass 1 of another (s1), interleaved 8
+// elements at a time in one instruction stream: pass 2's stores leave the SM at the pace of both
+// passes' arithmetic instead of in a burst per block (the SM's store path takes ~31 B/clk, less
+// than pass 2 alone produces), and each pass's dependent chains fill the other's latencies.
+// Exactly pass1_thread<V, true, false> and pass2_store_full<V, false>: the same operations on the
+// same values in the same per-thread order.  Returns the unclamped thread pair of s1.
+template <typename In>
+__device__ __forceinline__ Pair fused_pass1_pass2(const In* s1, const In* s2, float4 st, float* yb) {
+    constexpr int V = InTraits<In>::V;
+    const Pass2Consts k = pass2_consts(st.x, st.y);
+    AccV acc = accv_init();
+#pragma unroll kResUnroll  // one basic block per group: ptxas otherwise schedules every store of the block after the arithmetic
+    for (int g = 0; g < kPerThread / 8; ++g) {
+        float x2[8], x1[8], o[8];
+        load_group8<In>(s2, g, x2);
+        load_group8<In>(s1, g, x1);
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+            const float2 y = pass2_pair<false>(make_float2(x2[q], x2[q + 1]), k);
+            o[q] = y.x;
+            o[q + 1] = y.y;
+        }
+#pragma unroll
+        for (int h = 0; h < 8; h += 4)
+            // volatile: issued here, between the groups (the compiler otherwise sinks a block's stores to the end)
+            asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yb + vec_off<V>((int)threadIdx.x, (8 / V) * g + h / V) + (h % V)),
+                         "f"(o[h]), "f"(o[h + 1]), "f"(o[h + 2]), "f"(o[h + 3])
+                         : "memory");
+        float2 m[4], v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ext_exp2v<false>(make_float2(x1[2 * j], x1[2 * j + 1]), m[j], v[j]);
+        acc_add8v(acc, m, v);
+    }
+    return accv_pair(acc);
+}
 
 template <typename In>
 __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, int G, int ngroups, int nbuf, int ahead) {
@@ -81,8 +146,9 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
     __syncthreads();
     const unsigned long long tag = (unsigned long long)(s_epoch + 1u) << 32;  // this launch's tag
     const int64_t nrows = (a.rows - grp + ngroups - 1) / ngroups;  // the group's rows: grp + k ngroups
-    auto slot = [&](int64_t k, int j) { return stages + ((size_t)(k % nbuf) * nloc + j) * kBlockElems; };
-    auto ph = [&](int64_t k) { return (uint32_t)((k / nbuf) & 1); };  // phase parity of row k's use
+    const ResDiv ring(nbuf);
+    auto slot = [&](int64_t k, int j) { return stages + ((size_t)ring.rem(k) * nloc + j) * kBlockElems; };
+    auto ph = [&](int64_t k) { return (uint32_t)(ring.quot(k) & 1); };  // phase parity of row k's use
     // block value slots: (bits(m) | tag, bits(n) | tag), two single-copy-atomic 64-bit words
     unsigned long long* slots = reinterpret_cast<unsigned long long*>(a.ws + a.lay.res_vals);
 
@@ -94,7 +160,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
                 const int64_t row = grp + k * ngroups;
                 const int64_t e0 = (int64_t)(q + j * G) * kBlockElems;
                 const uint32_t bytes = (uint32_t)min((int64_t)kBlockElems, a.cols - e0) * (uint32_t)sizeof(In);
-                uint64_t* fb = &full_bar[(k % nbuf) * nloc + j];
+                uint64_t* fb = &full_bar[ring.rem(k) * nloc + j];
                 mbar_arrive_expect_tx(fb, bytes);
                 tma_load_1d(slot(k, j), x + row * a.cols + e0, bytes, fb, pol);
             };
@@ -102,7 +168,8 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
                 for (int j = 0; j < nloc; ++j) stage_in(k, j);
             for (int64_t k = 0; k + nbuf < nrows; ++k)
                 for (int j = 0; j < nloc; ++j) {  // pass 2 of row k has read the stage
-                    if (!wait_or_abort(&empty_bar[(k % nbuf) * nloc + j], ph(k), err, 2u)) return;
+                    if (!((TP_RES_EXP & 1) ? wait_sleep_or_abort(&empty_bar[ring.rem(k) * nloc + j], ph(k), err, 2u)
+                                           : wait_or_abort(&empty_bar[ring.rem(k) * nloc + j], ph(k), err, 2u))) return;
                     fence_proxy_async_smem();
                     stage_in(k + nbuf, j);
                 }
@@ -110,10 +177,11 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
     };
     auto post_role = [&]() {  // ------------------------------------------------------ post warp
         for (int64_t k = 0; k < nrows; ++k) {
-            const int b = (int)(k % nbuf);
+            const int b = ring.rem(k);
             const int64_t row = grp + k * ngroups;
             for (int j = 0; j < nloc; ++j) {
-                if (!wait_or_abort(&p1_bar[b * nloc + j], ph(k), err, 32u)) return;
+                if (!((TP_RES_EXP & 1) ? wait_sleep_or_abort(&p1_bar[b * nloc + j], ph(k), err, 32u)
+                                       : wait_or_abort(&p1_bar[b * nloc + j], ph(k), err, 32u))) return;
                 // block value: perfect tree over the 16 warp values in warp order (lanes 16-31
                 // identities: merge(v, identity) == v), as block_tree_warps
                 Pair v = lane < kWarps ? wparts[b * nloc + j][lane] : pair_identity();
@@ -128,7 +196,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
     };
     auto stats_role = [&]() {  // ------------------------------------------------ statistics warps
         for (int64_t k = warp - kResStatsWarp; k < nrows; k += 2) {
-            const int b = (int)(k % nbuf);
+            const int b = ring.rem(k);
             const int64_t row = grp + k * ngroups;
             // every lane loads its leaves' tagged words until all of the row's nb carry this
             // launch's tag: the poll is the load of the values (one round trip once they are in)
@@ -168,21 +236,24 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
     };
 
     // ------------------------------------------------------------------------ compute warps
-    auto pass1 = [&](int64_t k) -> bool {  // pass 1 of this warp's share of row k
-        const int b = (int)(k % nbuf);
-        for (int j = 0; j < nloc; ++j) {
-            if (!wait_or_abort(&full_bar[b * nloc + j], ph(k), err, 4u)) return false;
-            const int valid = (int)min((int64_t)kBlockElems, a.cols - (int64_t)(q + j * G) * kBlockElems);
-            BlockVals v;
-            load_stage<In>(slot(k, j), v);
-            Pair wp;
-            const bool cl = warp_pass1<V>(v, valid, &wp);
-            if (lane == 0) {
-                wparts[b * nloc + j][warp] = wp;
-                cbits[b * nloc + j][warp] = cl ? 1 : 0;
-                mbar_arrive(&p1_bar[b * nloc + j]);  // release: the warp value before the arrival
-            }
+    auto pass1_block = [&](int64_t k, int j) -> bool {  // pass 1 of this warp's share of block j of row k
+        const int b = ring.rem(k);
+        if (!wait_or_abort(&full_bar[b * nloc + j], ph(k), err, 4u)) return false;
+        const int valid = (int)min((int64_t)kBlockElems, a.cols - (int64_t)(q + j * G) * kBlockElems);
+        BlockVals v;
+        load_stage<In>(slot(k, j), v);
+        Pair wp = Pair{1.0f, 0.0f};
+        const bool cl = (TP_RES_EXP & 8) ? false : warp_pass1<V>(v, valid, &wp);
+        if (lane == 0) {
+            wparts[b * nloc + j][warp] = wp;
+            cbits[b * nloc + j][warp] = cl ? 1 : 0;
+            mbar_arrive(&p1_bar[b * nloc + j]);  // release: the warp value before the arrival
         }
+        return true;
+    };
+    auto pass1 = [&](int64_t k) -> bool {
+        for (int j = 0; j < nloc; ++j)
+            if (!pass1_block(k, j)) return false;
         return true;
     };
     // pass 1 runs `ahead` rows before pass 2: the group exchange of row k (the slowest CTA of the
@@ -192,19 +263,50 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
         for (int64_t k = 0; k < ahead && k < nrows; ++k)
             if (!pass1(k)) return;
         for (int64_t k = 0; k < nrows; ++k) {
-            if (k + ahead < nrows && !pass1(k + ahead)) return;
-            const int b = (int)(k % nbuf);
-            if (!wait_or_abort(&stats_bar[b], ph(k), err, 16u)) return;
-            const float4 st = make_float4(s_st[b].x, s_st[b].y, 0.f, 0.f);
+            const int b = ring.rem(k);
+            const bool more = k + ahead < nrows;
+            const int b1 = ring.rem(k + ahead);
+            if (!kResFuse && more && !pass1(k + ahead)) return;
+            if (!(TP_RES_EXP & 2) && !wait_or_abort(&stats_bar[b], ph(k), err, 16u)) return;
+            const float4 st = (TP_RES_EXP & 2) ? make_float4(3.0f, 0.25f, 0.f, 0.f) : make_float4(s_st[b].x, s_st[b].y, 0.f, 0.f);
             const int64_t row = grp + k * ngroups;
             for (int j = 0; j < nloc; ++j) {  // pass 2 on the staged blocks
                 const int64_t e0 = (int64_t)(q + j * G) * kBlockElems;
                 const int valid = (int)min((int64_t)kBlockElems, a.cols - e0);
+                const bool clamp = cbits[b * nloc + j][warp] != 0;
+                if (kResFuse && more) {  // with pass 1 of block j of row k + ahead
+                    if (!wait_or_abort(&full_bar[b1 * nloc + j], ph(k + ahead), err, 4u)) return;
+                    if (valid == kBlockElems && !clamp) {
+                        Pair acc = fused_pass1_pass2<In>(slot(k + ahead, j), slot(k, j), st, a.y + row * a.cols + e0);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty_bar[b * nloc + j]);
+                        const bool cl = __any_sync(0xffffffffu, acc_out_of_domain(acc));
+                        if (cl) {  // reading G11: the warp's values again, clamped
+                            BlockVals v1;
+                            load_stage<In>(slot(k + ahead, j), v1);
+                            acc = pass1_thread<V, false, true>(v1, valid);
+                        }
+                        const Pair wp = warp_value(acc);
+                        if (lane == 0) {
+                            wparts[b1 * nloc + j][warp] = wp;
+                            cbits[b1 * nloc + j][warp] = cl ? 1 : 0;
+                            mbar_arrive(&p1_bar[b1 * nloc + j]);
+                        }
+                        continue;
+                    }
+                    if (!pass1_block(k + ahead, j)) return;
+                }
                 BlockVals v;
                 load_stage<In>(slot(k, j), v);
-                const bool clamp = cbits[b * nloc + j][warp] != 0;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[b * nloc + j]);  // the stage may take the row nbuf ahead
+                if (TP_RES_EXP & 4) {  // arithmetic without the stores
+                    if (!(TP_RES_EXP & 16)) pass2_thread<false, V>(v, st.x, st.y);
+                    float sum = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < kPerThread; ++i) sum += v.v[i];
+                    if (sum == 123.456f) store_block<V>(a.y + row * a.cols + e0, valid, true, v);
+                } else
                 op_pass2<V>(v, st, clamp, a.y + row * a.cols + e0, valid, true);
             }
         }
@@ -231,7 +333,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres_kernel(const KArgs a, i
 template <typename In>
 int rowres_choose(int64_t rows, int64_t nb, int sms, int force_g) {
     constexpr int B = res_max_local<In>();
-    if (nb < 4 || nb > kResMaxNb || rows < 1) return 0;
+    if (nb < 4 || nb > kResMaxNb || rows < 1 || rows >= kResMaxRowsPerGroup) return 0;
     const int gmin = (int)((nb + B - 1) / B);
     if (force_g > 0) return force_g >= gmin && force_g <= nb && force_g <= sms ? force_g : 0;
     if (res_nbuf<In>(1) < 5 || nb > sms || rows < 2 * (sms / nb)) return 0;
@@ -246,7 +348,7 @@ cudaError_t launch_rowres(KArgs a, int G, const LaunchOpts& o, cudaStream_t s) {
     if (G < 1 || a.nb > kResMaxNb || (a.nb + G - 1) / G > res_max_local<In>() || !a.ws) return cudaErrorNotSupported;
     int64_t ngroups = (o.grid_ctas > 0 ? o.grid_ctas : sms) / G;
     if (ngroups > a.rows) ngroups = a.rows;
-    if (ngroups < 1) return cudaErrorNotSupported;
+    if (ngroups < 1 || (a.rows + ngroups - 1) / ngroups >= kResMaxRowsPerGroup) return cudaErrorNotSupported;
     const int per = (int)((a.nb + G - 1) / G);
     const int nbuf = res_nbuf<In>(per);
     const size_t dyn = (size_t)nbuf * per * kBlockElems * sizeof(In);

@@ -34,6 +34,20 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
     return v;
 }
 
+// k / d and k % d for the staging ring (d = rows staged, 2..8; k = a group's row index, < 2^29:
+// launch_rowres* refuse more rows per group) by one multiply-high with a magic computed once per
+// thread.  The 64-bit `k % nbuf`, `k / nbuf` by a runtime divisor used here first are subroutines
+// of ~100 dependent instructions, several per row on every compute warp at once: measured,
+// C4 bf16 300 -> see DESIGN (they were 13% of the kernel's stall samples).
+constexpr int64_t kResMaxRowsPerGroup = (int64_t)1 << 29;
+struct ResDiv {
+    unsigned magic;
+    int d;
+    __device__ __forceinline__ explicit ResDiv(int d_) : magic(0xffffffffu / (unsigned)d_ + 1u), d(d_) {}
+    __device__ __forceinline__ int quot(int64_t k) const { return (int)__umulhi((unsigned)k, magic); }
+    __device__ __forceinline__ int rem(int64_t k) const { return (int)((unsigned)k - (unsigned)quot(k) * (unsigned)d); }
+};
+
 constexpr int kResPostWarp = kWarps, kResStatsWarp = kWarps + 1, kResLoadWarp = kWarps + 3;
 
 }  // namespace tp

@@ -55,9 +55,10 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres3_kernel(const KArgs a, 
     __syncthreads();
     const unsigned long long tag = (unsigned long long)(s_epoch + 1u) << 32;
     const int64_t nrows = (a.rows - grp + ngroups - 1) / ngroups;
-    auto slot = [&](int64_t k, int j) { return stages + ((size_t)(k % nbuf) * nloc + j) * kBlockElems; };
-    auto si = [&](int64_t k, int j) { return (int)(k % nbuf) * nloc + j; };
-    auto ph = [&](int64_t k) { return (uint32_t)((k / nbuf) & 1); };
+    const ResDiv ring(nbuf);
+    auto slot = [&](int64_t k, int j) { return stages + ((size_t)ring.rem(k) * nloc + j) * kBlockElems; };
+    auto si = [&](int64_t k, int j) { return ring.rem(k) * nloc + j; };
+    auto ph = [&](int64_t k) { return (uint32_t)(ring.quot(k) & 1); };
     auto rowof = [&](int64_t k) { return grp + k * ngroups; };
     unsigned long long* slots = reinterpret_cast<unsigned long long*>(a.ws + a.lay.res_vals);
     const int span = kRecomp ? 2 * ahead : ahead;  // iterations from a row's max pass to its last read of x
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres3_kernel(const KArgs a, 
                     return;
                 }
             }
-            const int b = (int)(k % nbuf);
+            const int b = ring.rem(k);
             const float2 root = warp_reduce_leaves(w == 0 ? kRedMax : kRedSum, nb,
                                                    [&](int64_t j) { return make_float2(j == l0 ? f0 : f1, 0.0f); });
             if (w == 0) {
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres3_kernel(const KArgs a, 
             }
             const int64_t k1 = k - ahead;
             if (k1 >= 0 && k1 < nrows) {  // Sum-exp pass of row k1
-                const int b = (int)(k1 % nbuf);
+                const int b = ring.rem(k1);
                 if (!wait_or_abort(&mu_bar[b], ph(k1), err, 16u)) return;
                 const float mu = s_mu[b];
                 for (int j = 0; j < nloc; ++j) {
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(kResThreads, 1) rowres3_kernel(const KArgs a, 
             }
             const int64_t k2 = k - span;
             if (k2 >= 0 && k2 < nrows) {  // output pass of row k2
-                const int b = (int)(k2 % nbuf);
+                const int b = ring.rem(k2);
                 if (!wait_or_abort(&sg_bar[b], ph(k2), err, 16u)) return;
                 const float4 st = make_float4(s_mu[b], s_isg[b], 0.f, 0.f);
                 for (int j = 0; j < nloc; ++j) {
@@ -236,7 +237,7 @@ cudaError_t launch_rowres3(KArgs a, int G, const LaunchOpts& o, cudaStream_t s) 
     if (G < 1 || a.nb > kResMaxNb || (a.nb + G - 1) / G > res_max_local<In>() || !a.ws) return cudaErrorNotSupported;
     int64_t ngroups = (o.grid_ctas > 0 ? o.grid_ctas : sms) / G;
     if (ngroups > a.rows) ngroups = a.rows;
-    if (ngroups < 1) return cudaErrorNotSupported;
+    if (ngroups < 1 || (a.rows + ngroups - 1) / ngroups >= kResMaxRowsPerGroup) return cudaErrorNotSupported;
     const int per = (int)((a.nb + G - 1) / G);
     const int nbuf = res_nbuf<In>(per);
     const size_t dyn = (size_t)nbuf * per * kBlockElems * sizeof(In);

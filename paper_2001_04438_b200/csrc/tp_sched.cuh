@@ -310,6 +310,24 @@ __device__ __forceinline__ bool wait_or_abort(uint64_t* bar, uint32_t parity, un
     }
 }
 
+// The same for a service warp that waits most of the time: it sleeps between polls, so that its
+// polling does not take issue slots from the compute warps of its scheduler.
+__device__ __forceinline__ bool wait_sleep_or_abort(uint64_t* bar, uint32_t parity, unsigned* err, unsigned bit) {
+    if (mbar_try_parity(bar, parity)) return true;
+    const unsigned long long t0 = globaltimer_ns();
+    for (unsigned i = 1;; ++i) {
+        __nanosleep(64);
+        if (mbar_try_parity(bar, parity)) return true;
+        if ((i & 63u) == 0) {
+            if (*reinterpret_cast<volatile unsigned*>(err)) return false;
+            if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                raise_abort(err, bit);
+                return false;
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ bool aborted(unsigned* err) { return *reinterpret_cast<volatile unsigned*>(err) != 0; }
 
 __device__ __forceinline__ void exit_and_reset(WsHeader* hdr) {
